@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""Benchmark: Ozaki-scheme FP8 DGEMM on B200 (FP64-equivalent TFLOPS).
+
+Metric (BASELINE.json): FP64-equivalent TFLOPS = 2*m*n*k / t of the Ozaki-FP8
+DGEMM at n = 8192, phi = 0.5, reference options (all slice pairs, smallest-
+first, hardware FP64 accumulation), next to native cuBLAS DGEMM on the same
+GPU, with max relative error against a double-double oracle.
+
+One step = one full oz_gemm over resident A, B (split A and B, fused slice-pair
+GEMM + accumulation).  A and B are 512 MiB each, larger than the 126 MB L2, so
+no explicit flush is needed between steps.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N > 1 (torchrun): 2-D output-tile sharding — each rank owns one n x n tile of
+a (R*n) x (Cc*n) C, its A row-panel and B column-panel broadcast once per step
+over NCCL from the row-/column-group roots (weak scaling: per-GPU work fixed).
+--impl reference times the reference algorithm on the host cores (the C
+restatement under oracle/; the reference itself is pure Python/numpy).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "FP64-equiv TFLOPS, Ozaki-FP8 DGEMM n=8192 vs native DGEMM; max rel error"
+UNIT = "TFLOP/s (FP64-equivalent)"
+KERNELS_PER_BLOCK = 8  # split_count x2, transpose, split_rows x2, tile_counts x2, pair_gemm
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--phi", type=float, default=0.5)
+    ap.add_argument("--type2", default="fp8e4m3")
+    ap.add_argument("--type3", default="fp32")
+    ap.add_argument("--kblock", type=int, default=0)
+    ap.add_argument("--emu", action="store_true")
+    ap.add_argument("--max-slices", type=int, default=None)
+    ap.add_argument("--pair-cutoff", type=int, default=None)
+    ap.add_argument("--no-skip", action="store_true", help="disable (result-neutral) zero-pair skipping")
+    ap.add_argument("--no-extras", action="store_true", help="skip accuracy / cuBLAS / CPU-baseline legs")
+    ap.add_argument("--cpu-rows", type=int, default=64, help="CPU-baseline sample: rows of C")
+    ap.add_argument("--cpu-cols", type=int, default=512, help="CPU-baseline sample: cols of C")
+    ap.add_argument("--acc-rows", type=int, default=256, help="rows of C checked against the DD oracle")
+    return ap.parse_args()
+
+
+def make_inputs(n_rows, n_k, n_cols, phi, seed):
+    """(rand - 0.5) * exp(phi * randn), numpy PCG64, A then B."""
+    rng = np.random.default_rng(seed)
+    A = (rng.random((n_rows, n_k)) - 0.5) * np.exp(phi * rng.standard_normal((n_rows, n_k)))
+    B = (rng.random((n_k, n_cols)) - 0.5) * np.exp(phi * rng.standard_normal((n_k, n_cols)))
+    return A, B
+
+
+def gpu_inputs(torch, m, k, n, phi, seed, device):
+    """Same formula generated on the device (fast for large n)."""
+    g = torch.Generator(device=device).manual_seed(seed)
+    A = (torch.rand((m, k), generator=g, device=device, dtype=torch.float64) - 0.5) * torch.exp(
+        phi * torch.randn((m, k), generator=g, device=device, dtype=torch.float64))
+    B = (torch.rand((k, n), generator=g, device=device, dtype=torch.float64) - 0.5) * torch.exp(
+        phi * torch.randn((k, n), generator=g, device=device, dtype=torch.float64))
+    return A, B
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        rows = []
+        try:
+            for line in Path(self.path).read_text().splitlines():
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 8 and f[1].replace(".", "").isdigit():
+                    rows.append(f)
+        finally:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"bf16": d.get("bf16_tflops"), "bf16_sustained": d.get("bf16_tflops_sustained"),
+                "hbm": d.get("hbm_gbs"), "source": "MEASURED_PEAKS.json"}
+    return {"bf16": 1590.0, "bf16_sustained": 1400.0, "hbm": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def executed_pairs(tca, tcb, sx, sy, cutoff):
+    """MMA pairs the fused kernel actually runs (per-tile zero-pair skipping)."""
+    ha = np.bincount(np.minimum(tca, sx), minlength=sx + 1)
+    hb = np.bincount(np.minimum(tcb, sy), minlength=sy + 1)
+    tot = 0
+    for lp in range(sx + 1):
+        if not ha[lp]:
+            continue
+        for lq in range(sy + 1):
+            if not hb[lq]:
+                continue
+            if cutoff is None:
+                cnt = lp * lq
+            else:
+                cnt = sum(1 for p in range(lp) for q in range(lq) if p + q <= cutoff)
+            tot += int(ha[lp]) * int(hb[lq]) * cnt
+    return tot
+
+
+def cpu_baseline(args, rows, cols, n, threads=None):
+    """Reference algorithm (C restatement, oracle/) on the host cores for a
+    bounded sample: rows x cols of C at the full inner dimension n (same k, phi
+    and options as the GPU workload, so the slice structure matches)."""
+    import oracle
+
+    A, B = make_inputs(rows, n, cols, args.phi, 1234)
+    threads = threads or oracle.max_threads()
+    t0 = time.perf_counter()
+    _, info = oracle.oz_gemm(A, B, args.type2, args.type3, args.kblock, args.emu, args.max_slices,
+                             "smallest-first", args.pair_cutoff, nthreads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": 2.0 * rows * cols * n / dt / 1e12, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"C[{rows}x{cols}] at k={n}, phi={args.phi}, {args.type2}/{args.type3} "
+                      f"(reference algorithm, C restatement oracle/oz_oracle.c, {threads} threads)",
+            "seconds": dt, "blocks": info["blocks"]}
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+
+    oracle.build()
+    n = args.n
+    rows, cols = args.cpu_rows, args.cpu_cols
+    threads = oracle.max_threads()
+    for _ in range(args.warmup):
+        cpu_baseline(args, rows, cols, n, threads)
+    times = [cpu_baseline(args, rows, cols, n, threads) for _ in range(args.steps)]
+    vals = [t["value"] for t in times]
+    v = statistics.median(vals)
+    ms = statistics.median([t["seconds"] for t in times]) * 1e3
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64 (fp32 slice products)", "data": "synthetic",
+           "impl": "reference",
+           "config": workload_config(args, per_gpu=True),
+           "cpu_baseline": {k: times[0][k] for k in ("unit", "cores", "kind", "sample")} | {"value": v},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def workload_config(args, per_gpu=False):
+    opts = []
+    if args.emu:
+        opts.append("integer-emulated FP64")
+    if args.max_slices:
+        opts.append(f"max_slices={args.max_slices}")
+    if args.pair_cutoff is not None:
+        opts.append(f"pair_cutoff={args.pair_cutoff}")
+    if args.kblock:
+        opts.append(f"k_block={args.kblock}")
+    return {"workload": f"Ozaki-{args.type2} DGEMM m=n=k={args.n} phi={args.phi} "
+                        + (", ".join(opts) if opts else "reference defaults (all pairs, smallest-first, HW FP64)"),
+            "m": args.n, "n": args.n, "k": args.n, "phi": args.phi, "type2": args.type2, "type3": args.type3,
+            "k_block": args.kblock, "fp64_emulation": args.emu, "max_slices": args.max_slices,
+            "pair_cutoff": args.pair_cutoff, "skip_zero_pairs": not args.no_skip,
+            "l2": "inputs (2 x 512 MiB at n=8192) exceed the 126 MB L2; no flush",
+            "parallelism": "2-D C tiles" if args.gpus > 1 else "1 GPU"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_00441_b200 as oz
+    from paper_2508_00441_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = args.n
+    cfg = oz.GemmConfig(oz.get_format(args.type2), oz.get_format(args.type3), k_block=args.kblock,
+                        fp64_emulation=args.emu, max_slices=args.max_slices, pair_cutoff=args.pair_cutoff,
+                        skip_zero_pairs=not args.no_skip)
+
+    # ---- inputs: this rank's C tile is n x n; A row-panel n x n, B column-panel n x n ----
+    from paper_2508_00441_b200.distributed import TileGrid
+
+    grid = TileGrid.for_world(world)
+    ti, tj = grid.coords(rank)
+    A = torch.empty((n, n), dtype=torch.float64, device=dev)
+    B = torch.empty((n, n), dtype=torch.float64, device=dev)
+    if grid.is_row_root(rank):
+        A.copy_(gpu_inputs(torch, n, n, 8, args.phi, 1000 + ti, dev)[0])
+    if grid.is_col_root(rank):
+        B.copy_(gpu_inputs(torch, 8, n, n, args.phi, 2000 + tj, dev)[1])
+    groups = grid.make_groups(dist) if world > 1 else None
+
+    def step():
+        if world > 1:
+            grid.distribute_panels(dist, groups, rank, A, B)
+        C, st = oz.oz_gemm_device(A, B, cfg, out=Cbuf)
+        return st
+
+    Cbuf = torch.empty((n, n), dtype=torch.float64, device=dev)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    gemm_s, slice_s = [], []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev[0].record()
+        for i in range(args.steps):
+            st = step()
+            ev[i + 1].record()
+            gemm_s.append(st.t_gemm)
+            slice_s.append(st.t_slice)
+        torch.cuda.synchronize()
+    clocks = clk.summary()
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    tot_ms = ev[0].elapsed_time(ev[-1])
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        dist.barrier()
+    flops_per_gpu = 2.0 * n * n * n
+    value = world * flops_per_gpu * args.steps / (tot_ms / 1e3) / 1e12
+
+    # Executed MMA work of the dominant kernel (for the roofline).
+    blk = st.blocks[0]
+    from paper_2508_00441_b200.slicing import split_rows_device, transpose_device
+
+    params = oz.compute_params(53, cfg.type2.mant_bits, cfg.type3.mant_bits, n)
+    sa, _ = split_rows_device(A, cfg.type2, params, args.emu)
+    sb, _ = split_rows_device(transpose_device(B), cfg.type2, params, args.emu)
+    tca = sa.row_cnt.view(-1, 128).max(dim=1).values.cpu().numpy() if n % 128 == 0 else None
+    tcb = sb.row_cnt.view(-1, 128).max(dim=1).values.cpu().numpy() if n % 128 == 0 else None
+    if cfg.skip_zero_pairs and tca is not None:
+        pairs_exec = executed_pairs(tca, tcb, blk.s_x, blk.s_y, args.pair_cutoff) / (len(tca) * len(tcb))
+    else:
+        pairs_exec = blk.gemms
+    del sa, sb
+    mma_flops = 2.0 * n * n * n * pairs_exec
+    gemm_ms = statistics.mean(gemm_s) * 1e3
+    peaks = measured_peaks()
+    fp8_peak = 2.0 * peaks["bf16"]
+    achieved = mma_flops / (gemm_ms / 1e3) / 1e12
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": fp8_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp8_peak, "traffic": None,
+                "kernel": "pair_gemm_kernel<false> (fused slice-pair GEMM + FP64 accumulation)",
+                "peak_source": f"dense fp8 = 2 x measured dense bf16 ({peaks['source']})",
+                "algorithmic_flops_per_launch": mma_flops,
+                "pairs_per_tile_executed_mean": pairs_exec, "pairs_reference": blk.gemms,
+                "kernel_ms": gemm_ms, "split_ms": statistics.mean(slice_s) * 1e3}
+
+    extras = {}
+    if rank == 0 and not args.no_extras:
+        extras = run_extras(args, torch, oz, A, B, cfg, dev)
+    # ---- e2e through the public API with host buffers (pinned) ----
+    Ah = A.cpu().pin_memory()
+    Bh = B.cpu().pin_memory()
+    oz.oz_gemm(Ah, Bh, cfg)
+    torch.cuda.synchronize()
+    e2e_t = []
+    for _ in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        r = oz.oz_gemm(Ah, Bh, cfg)
+        torch.cuda.synchronize()
+        e2e_t.append(time.perf_counter() - t0)
+        del r
+    e2e_v = world * flops_per_gpu / statistics.median(e2e_t) / 1e12
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64 (fp8 e4m3 slice products)"
+               if args.type2 == "fp8e4m3" else f"f64 ({args.type2} slice products)",
+               "data": "synthetic (rand-0.5)*exp(phi*randn), generated on device",
+               "config": workload_config(args),
+               "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * n * n,
+                       "d2h_bytes_per_step": 8 * n * n, "path": "oz_gemm(pinned host tensors) -> host C"},
+               "gpu_launches": KERNELS_PER_BLOCK * len(st.blocks) * args.steps,
+               "roofline": roofline, "clocks": clocks,
+               "slices": {"s_x": blk.s_x, "s_y": blk.s_y, "gemm_count": st.gemm_count},
+               "step_ms": step_ms}
+        out.update(extras)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_extras(args, torch, oz, A, B, cfg, dev):
+    """Accuracy vs the DD oracle, native cuBLAS DGEMM / FP8 on the same GPU,
+    and the CPU baseline (rank 0, N=1 leg)."""
+    from paper_2508_00441_b200 import _lib
+
+    n = args.n
+    out = {}
+    # native DGEMM
+    C64 = torch.matmul(A, B)
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e[0].record()
+    reps = 3
+    for _ in range(reps):
+        C64 = torch.matmul(A, B)
+    e[1].record()
+    torch.cuda.synchronize()
+    dg_ms = e[0].elapsed_time(e[1]) / reps
+    out["native_dgemm"] = {"tflops": 2.0 * n ** 3 / (dg_ms / 1e3) / 1e12, "ms": dg_ms,
+                           "impl": "torch.matmul float64 (cuBLAS)"}
+    # cuBLAS FP8 dense peak reference
+    try:
+        a8 = torch.randn((8192, 8192), device=dev).to(torch.float8_e4m3fn)
+        b8 = torch.randn((8192, 8192), device=dev).to(torch.float8_e4m3fn).t()
+        one = torch.ones((), device=dev)
+        torch._scaled_mm(a8, b8, one, one, out_dtype=torch.bfloat16)
+        torch.cuda.synchronize()
+        e[0].record()
+        for _ in range(10):
+            torch._scaled_mm(a8, b8, one, one, out_dtype=torch.bfloat16)
+        e[1].record()
+        torch.cuda.synchronize()
+        out["cublas_fp8_tflops"] = 2.0 * 8192 ** 3 / (e[0].elapsed_time(e[1]) / 10 / 1e3) / 1e12
+        del a8, b8
+    except Exception as ex:  # noqa: BLE001
+        out["cublas_fp8_tflops"] = f"unavailable: {ex}"
+    # accuracy on a row sample vs double-double oracle
+    r = args.acc_rows
+    Cdd = torch.empty((r, n), dtype=torch.float64, device=dev)
+    _lib.call("oz_dd_gemm", A[:r].contiguous().data_ptr(), B.data_ptr(), Cdd.data_ptr(), r, n, n,
+              _lib.stream_ptr(torch))
+    Coz, _ = oz.oz_gemm_device(A[:r].contiguous(), B, cfg)
+    torch.cuda.synchronize()
+
+    def relerr(X):
+        nz = Cdd != 0
+        return float(((X - Cdd).abs()[nz] / Cdd.abs()[nz]).max().item())
+
+    out["accuracy"] = {"rows_checked": r, "oracle": "double-double GEMM (oz_dd_gemm)",
+                       "max_rel_err_ozaki": relerr(Coz), "max_rel_err_cublas_dgemm": relerr(C64[:r])}
+    del C64, Cdd, Coz
+    out["cpu_baseline"] = cpu_baseline(args, args.cpu_rows, args.cpu_cols, n)
+    out["cpu_baseline"].pop("blocks", None)
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,115 @@
+/* oz_b200.h — C ABI of the B200 Ozaki-scheme DGEMM (liboz_b200.so).
+ *
+ * The reference (arxiv 2508.00441, package `ozdgemm`, pure Python/numpy) has no
+ * FFI; its drop-in boundary is the Python signature oz_gemm(A, B, cfg)
+ * (pkg/src/ozdgemm/ozgemm.py:143) and its internal seams slice_matrix
+ * (slicing.py:190), lp_gemm (lpgemm.py:93) and the pair-accumulation loop
+ * (ozgemm.py:179-209).  Each entry point below replaces one of those seams;
+ * the Python package paper_2508_00441_b200 binds them with ctypes and keeps the
+ * reference's Python API on top.
+ *
+ * Conventions
+ *   - all matrix pointers are DEVICE pointers, row-major, leading dimension in
+ *     elements; the library never allocates or frees caller memory;
+ *   - every call is asynchronous on `stream` (a cudaStream_t, NULL = legacy);
+ *   - kernels OR error bits into the device word *flags (OZ_FLAG_*); the caller
+ *     reads it after a stream sync and maps it to the reference's exceptions;
+ *   - return value: OZ_OK or an OZ_E* status (launch-time argument errors).
+ *
+ * type2 codes (slice storage format, formats.py:85-100):
+ *   OZ_FMT_E4M3 = 0 (fp8e4m3), OZ_FMT_E5M2 = 1 (fp8e5m2), OZ_FMT_FP16 = 2, OZ_FMT_BF16 = 3
+ */
+#ifndef OZ_B200_H
+#define OZ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  OZ_OK = 0,
+  OZ_EINVAL = 1,       /* bad argument (shape, pointer, format)              */
+  OZ_EUNSUPPORTED = 2, /* format/size combination not implemented on sm_100a */
+  OZ_ECUDA = 3,        /* CUDA runtime error at launch                        */
+  OZ_ETMAP = 4,        /* cuTensorMapEncodeTiled failed                      */
+  OZ_ESLICES = 5       /* more B slices than the epilogue stages (64)         */
+};
+
+enum { OZ_FMT_E4M3 = 0, OZ_FMT_E5M2 = 1, OZ_FMT_FP16 = 2, OZ_FMT_BF16 = 3 };
+
+/* device error-flag bits */
+#define OZ_FLAG_NONFINITE_INPUT (1u << 0)   /* slicing.py:120-121  -> ValueError        */
+#define OZ_FLAG_SUBNORMAL_INPUT (1u << 1)   /* slicing.py:122-125  -> RangeError        */
+#define OZ_FLAG_SIGMA_RANGE (1u << 2)       /* slicing.py:157-158  -> RangeError        */
+#define OZ_FLAG_SLICE_CAP (1u << 3)         /* > planes / 2100 slices -> AssertionError */
+#define OZ_FLAG_NOT_REPRESENTABLE (1u << 4) /* slicing.py:169-172  -> SlicingInfeasible */
+#define OZ_FLAG_EMU_RANGE (1u << 5)         /* fp64emu.py:240-241  -> RangeError        */
+#define OZ_FLAG_TERM_RANGE (1u << 6)        /* ozgemm.py:137-139   -> RangeError        */
+#define OZ_FLAG_SUBNORMAL_RESID (1u << 7)   /* fp64emu.py:73-82    -> RangeError        */
+
+/* Count pass of the row split — replaces the slice-count side of
+ * slicing._slice_rows (slicing.py:128-177): per-row slice counts row_cnt[rows],
+ * *s_max = max(*s_max, max_r row_cnt[r]) (the reference's s, slicing.py:206),
+ * plus input-validation flags (slicing.py:119-125).  X is rows x kb, ldx >= kb. */
+int oz_split_count(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2, int rho, int emu,
+                   int32_t* row_cnt, int32_t* s_max, uint32_t* flags, void* stream);
+
+/* Write pass — replaces slice_matrix(X, "rows", ...) (slicing.py:190-198):
+ * emits exactly `planes` slice planes coeff[p][rows][ld_coeff] (type2 codes,
+ * K-major; ld_coeff*elem_bytes must be a multiple of 16, padding zeroed) and
+ * expo[p][rows] (int32 c_p, 0 for exhausted rows).  `planes` must be >= the
+ * count pass's s. */
+int oz_split_rows(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2, int rho, int emu, int planes,
+                  void* coeff, int64_t ld_coeff, int32_t* expo, int32_t* row_cnt, uint32_t* flags, void* stream);
+
+/* dst (cols x rows, ld_dst) = transpose(src (rows x cols, ld_src)).  Used to
+ * slice B by columns (slice_matrix(..., "cols"), slicing.py:199-203) and as
+ * ozgemm.transpose (ozgemm.py:121-123). */
+int oz_transpose(const double* src, int64_t rows, int64_t cols, int64_t ld_src, double* dst, int64_t ld_dst,
+                 void* stream);
+
+/* tile_cnt[t] = max over rows [128t, 128t+128) of row_cnt — per-output-tile slice
+ * counts used to skip all-zero slice pairs (result-neutral). */
+int oz_tile_counts(const int32_t* row_cnt, int64_t rows, int32_t* tile_cnt, void* stream);
+
+/* Fused slice-pair GEMM + exact scaling + ordered FP64 accumulation for one
+ * inner-product block — replaces ozgemm.py:179-209 (pair order :179-183,
+ * lp_gemm :188-190, _scale_terms_exact :132-140/:192-193, Cb += T :194-197,
+ * C += Cb :204-207).
+ *   a_planes: >= sx planes [m][ld_a]; b_planes: >= sy planes [n][ld_b] (columns of
+ *   B as K-major rows); expo_a[p][m], expo_b[q][n]; tile_cnt_a/b may be NULL (no
+ *   pair skipping).  order: 0 smallest-first, 1 largest-first.  pair_cutoff < 0
+ *   keeps all pairs (reference semantics); >= 0 keeps p+q <= pair_cutoff
+ *   (opt-in extension).  emu: integer-only FP64 epilogue.  accumulate: 0 writes
+ *   C = Cb, 1 writes C = C + Cb. */
+int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64_t ld_b, int planes_a,
+                 int planes_b, const int32_t* expo_a, const int32_t* expo_b, const int32_t* tile_cnt_a,
+                 const int32_t* tile_cnt_b, int64_t m, int64_t n, int64_t kb, int sx, int sy, int type2,
+                 int order, int pair_cutoff, int emu, int accumulate, double* C, int64_t ldc, uint32_t* flags,
+                 void* stream);
+
+/* One slice-pair product D (m x n, fp32) = A (m x k) . B (n x k)^T on tcgen05 —
+ * replaces lpgemm.lp_gemm (lpgemm.py:93-120) for slice operands (exact). */
+int oz_lp_gemm(const void* a_plane, const void* b_plane, int64_t ld_a, int64_t ld_b, int64_t m, int64_t n,
+               int64_t k, int type2, float* D, int64_t ldd, void* stream);
+
+/* Accuracy harness (not on the product path): C = A . B with double-double
+ * accumulation (TwoProd/TwoSum) and one final rounding — stands in for the
+ * reference's exact oracle ref_gemm (oracle.py:150-174) at n >= 4096.
+ * A m x k, B k x n, C m x n, all row-major contiguous. */
+int oz_dd_gemm(const double* A, const double* B, double* C, int64_t m, int64_t n, int64_t k, void* stream);
+
+/* Human-readable status string. */
+const char* oz_strerror(int status);
+
+/* Library version string (also proves the .so loaded). */
+const char* oz_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OZ_B200_H */

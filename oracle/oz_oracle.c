@@ -1,0 +1,310 @@
+/* oz_oracle.c — CPU restatement of the reference Ozaki-scheme DGEMM hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This file is the parity checker for the CUDA path
+ * and the CPU baseline of bench.py; the product (paper_2508_00441_b200) never
+ * links or calls it.  It restates, in plain C, the algorithm of the reference
+ * package ozdgemm 1.0.0 (/root/reference/pkg/src/ozdgemm):
+ *
+ *   oro_emu_add        fp64emu._add_core            fp64emu.py:193-251
+ *   oro_split_rows     slicing._slice_rows          slicing.py:128-177
+ *                      (+ _validate_input :119-125, max_abs fp64emu.py:315-319,
+ *                       ceil_log2_abs :280-284, scale2 :269-277)
+ *   oro_pair_block     ozgemm.oz_gemm pair loop     ozgemm.py:179-209
+ *                      lp_gemm fast fp32 path       lpgemm.py:105-116
+ *                      _scale_terms_exact           ozgemm.py:132-140
+ *
+ * Pinned against golden vectors produced by the reference itself
+ * (tests/golden/gen_golden.py -> tests/golden/{name}.npz, checked by
+ * tests/test_oracle_golden.py).  Build: oracle/Makefile (gcc -O3
+ * -ffp-contract=off so every double/float operation is a single IEEE RNE op).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+#include <unistd.h>
+
+#define SIGN 0x8000000000000000ull
+#define EXPM 0x7FF0000000000000ull
+#define FRACM 0x000FFFFFFFFFFFFFull
+#define HID (1ull << 52)
+
+/* flag bits: identical to include/oz_b200.h */
+#define F_NONFINITE (1u << 0)
+#define F_SUBNORMAL_IN (1u << 1)
+#define F_SIGMA (1u << 2)
+#define F_CAP (1u << 3)
+#define F_EMU_RANGE (1u << 5)
+#define F_TERM (1u << 6)
+#define F_SUBNORMAL_RES (1u << 7)
+
+static inline uint64_t bits(double x) { uint64_t b; memcpy(&b, &x, 8); return b; }
+static inline double dbl(uint64_t b) { double x; memcpy(&x, &b, 8); return x; }
+
+static int operand_bad(uint64_t a) {
+  const uint64_t e = (a & EXPM) >> 52;
+  return e == 2047 || (e == 0 && (a & FRACM) != 0);
+}
+
+/* fp64emu._add_core: integer-only RNE addition of normal-or-zero operands. */
+uint64_t oro_emu_add(uint64_t a, uint64_t b, uint32_t* flags) {
+  if (operand_bad(a) || operand_bad(b)) *flags |= F_EMU_RANGE;
+  const int za = (a & ~SIGN) == 0, zb = (b & ~SIGN) == 0;
+  if (za && zb) return a & b & SIGN;
+  if (za) return b;
+  if (zb) return a;
+  const uint64_t maga = a & ~SIGN, magb = b & ~SIGN;
+  const uint64_t big = magb > maga ? b : a, sml = magb > maga ? a : b;
+  const int same = (a >> 63) == (b >> 63);
+  const int64_t eb = (int64_t)((big & EXPM) >> 52), es = (int64_t)((sml & EXPM) >> 52);
+  const uint64_t mb = ((big & FRACM) | HID) << 10;
+  uint64_t ms = ((sml & FRACM) | HID) << 10;
+  int64_t d = eb - es;
+  if (d > 63) d = 63;
+  if (d > 0) {
+    const uint64_t lost = ms & ((1ull << d) - 1);
+    ms = (ms >> d) | (lost ? 1ull : 0ull);
+  }
+  uint64_t mag = same ? mb + ms : mb - ms;
+  if (mag == 0) return 0; /* exact cancellation -> +0 */
+  int pos = 63;
+  while (!((mag >> pos) & 1)) --pos;
+  int64_t adj = 0;
+  if (pos == 63) { mag = (mag >> 1) | (mag & 1); adj = 1; }
+  else if (pos < 62) { mag <<= (62 - pos); adj = -(int64_t)(62 - pos); }
+  uint64_t sig = mag >> 10;
+  const uint64_t rem = mag & 1023;
+  if (rem > 512 || (rem == 512 && (sig & 1))) ++sig;
+  int64_t carry = 0;
+  if (sig == (1ull << 53)) { sig >>= 1; carry = 1; }
+  int64_t ex = eb + adj + carry;
+  if (ex < 1 || ex > 2046) { *flags |= F_EMU_RANGE; ex = ex < 1 ? 1 : 2046; }
+  return (big & SIGN) | ((uint64_t)ex << 52) | (sig & FRACM);
+}
+
+/* fp64emu._scale2_core on one value: exponent shift with range check. */
+static uint64_t emu_scale2(uint64_t a, int64_t t, uint32_t* flags) {
+  if ((a & ~SIGN) == 0) return a;
+  int64_t e = (int64_t)((a & EXPM) >> 52) + t;
+  if (e < 1 || e > 2046) { *flags |= F_EMU_RANGE; e = e < 1 ? 1 : 2046; }
+  return (a & ~EXPM) | ((uint64_t)e << 52);
+}
+
+/* Slice every row of X (rows x kb, ld ldx).  coeff: [cap][rows][kb] doubles,
+ * expo: [cap][rows].  Rows are independent in the reference loop (each
+ * iteration works per row; exhausted rows emit zero slices with c = 0), so
+ * each row is sliced to exhaustion and padded afterwards.  Returns s (the
+ * maximum row count) or -1 if a row needs more than `cap` slices. */
+int oro_split_rows(const double* X, int64_t rows, int64_t kb, int64_t ldx, int rho, int emu, int cap,
+                   double* coeff, int32_t* expo, int32_t* cnt, uint32_t* flags_out) {
+  uint32_t flags = 0;
+  int s = 0, over = 0;
+  double* x = (double*)malloc(sizeof(double) * (kb > 0 ? kb : 1));
+  /* _validate_input over the whole matrix first */
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t t = 0; t < kb; ++t) {
+      const uint64_t b = bits(X[r * ldx + t]);
+      const uint64_t e = (b & EXPM) >> 52;
+      if (e == 2047) flags |= F_NONFINITE;
+      else if (e == 0 && (b & ~SIGN)) flags |= F_SUBNORMAL_IN;
+    }
+  if (flags) { free(x); *flags_out |= flags; return 0; }
+  for (int64_t r = 0; r < rows; ++r) {
+    for (int64_t t = 0; t < kb; ++t) x[t] = X[r * ldx + t];
+    int it = 0;
+    for (;; ++it) {
+      uint64_t mx = 0;
+      for (int64_t t = 0; t < kb; ++t) {
+        const uint64_t b = bits(x[t]);
+        if (operand_bad(b)) flags |= F_SUBNORMAL_RES;
+        const uint64_t a = b & ~SIGN;
+        if (a > mx) mx = a;
+      }
+      if (mx == 0) break;
+      if (it >= 2100) { flags |= F_CAP; break; }
+      if (it >= cap) { over = 1; break; }
+      const int64_t e = (int64_t)(mx >> 52) - 1023;
+      const int64_t c = (mx & FRACM) ? e + 1 : e;
+      const int64_t se = c + rho - 1 + 1023;
+      if (se < 1 || se > 2046) { flags |= F_SIGMA; break; }
+      const double sigma = dbl(((uint64_t)se << 52) | (1ull << 51));
+      double* out = coeff + ((int64_t)it * rows + r) * kb;
+      for (int64_t t = 0; t < kb; ++t) {
+        double v;
+        if (emu) {
+          const uint64_t s1 = oro_emu_add(bits(x[t]), bits(sigma), &flags);
+          v = dbl(oro_emu_add(s1, bits(sigma) ^ SIGN, &flags));
+          x[t] = dbl(oro_emu_add(bits(x[t]), bits(v) ^ SIGN, &flags));
+          out[t] = dbl(emu_scale2(bits(v), -c, &flags));
+        } else {
+          v = (x[t] + sigma) - sigma;
+          x[t] = x[t] - v;
+          out[t] = ldexp(v, (int)-c);
+        }
+      }
+      expo[(int64_t)it * rows + r] = (int32_t)c;
+    }
+    cnt[r] = it;
+    if (it > s) s = it;
+  }
+  free(x);
+  *flags_out |= flags;
+  if (over) return -1;
+  for (int64_t r = 0; r < rows; ++r)
+    for (int p = cnt[r]; p < s; ++p) {
+      memset(coeff + ((int64_t)p * rows + r) * kb, 0, sizeof(double) * kb);
+      expo[(int64_t)p * rows + r] = 0;
+    }
+  return s;
+}
+
+/* Pair list in reference order (ozgemm.py:179-183), optional p+q <= cutoff. */
+static int build_pairs(int sx, int sy, int order, int cutoff, int* pp, int* qq) {
+  int n = 0;
+  const int dmax = sx + sy - 2;
+  for (int k = 0; k <= dmax; ++k) {
+    const int d = order == 0 ? dmax - k : k;
+    if (cutoff >= 0 && d > cutoff) continue;
+    for (int p = 0; p < sx; ++p) {
+      const int q = d - p;
+      if (q < 0 || q >= sy) continue;
+      pp[n] = p; qq[n] = q; ++n;
+    }
+  }
+  return n;
+}
+
+/* ldexp(G, e) with the reference's HW-mode range rule (ozgemm.py:132-140) or
+ * fp64emu.scale2 (emu).  Returns the term bits. */
+static uint64_t scale_term(double g, int64_t e, int emu, uint32_t* flags) {
+  if (emu) return emu_scale2(bits(g), e, flags);
+  const double t = ldexp(g, (int)(e > 4000 ? 4000 : e < -4000 ? -4000 : e));
+  const uint64_t b = bits(t);
+  const uint64_t ex = (b & EXPM) >> 52;
+  if (ex == 2047 || (ex == 0 && (b & ~SIGN))) *flags |= F_TERM;
+  return b;
+}
+
+/* One inner-product block of oz_gemm.  coeffA: [>=sx][m][kb] (rows of A),
+ * coeffB: [>=sy][kb][n] (the reference's column-slice matrices).  fp32: 1 to
+ * accumulate G in float with per-step RNE (the reference fast path), 0 for
+ * double (exact; used when type3 != fp32).  C = Cb (accumulate == 0) or
+ * C = C + Cb.  Rows are independent, so row blocks are spread over pthreads;
+ * every element still sees the exact reference sequence of operations. */
+typedef struct {
+  const double* coeffA; const int32_t* expoA; const double* coeffB; const float* Bf; const int32_t* expoB;
+  int64_t m, n, kb; const int* pp; const int* qq; int np; int emu, fp32, accumulate; double* C;
+  int64_t next_block; pthread_mutex_t mu; uint32_t flags;
+} BlockJob;
+
+#define RB 16
+
+#define CB 256
+
+/* Rows [r0, r0+RB) x columns [c0, c0+CB) of C; n below is the chunk width. */
+static void block_rows(BlockJob* J, int64_t r0, int64_t c0, double* Cb, float* gf, double* gd, uint32_t* flags) {
+  const int64_t m = J->m, N = J->n, kb = J->kb;
+  const int64_t rb = (m - r0) < RB ? (m - r0) : RB;
+  const int64_t n = (N - c0) < CB ? (N - c0) : CB;
+  for (int64_t i = 0; i < rb * n; ++i) Cb[i] = 0.0;
+  for (int pi = 0; pi < J->np; ++pi) {
+    const int p = J->pp[pi], q = J->qq[pi];
+    const double* Ap = J->coeffA + (int64_t)p * m * kb;
+    /* G rows r0..r0+rb: ascending-t rank-1 updates (lpgemm.py:112-113) */
+    if (J->fp32) {
+      const float* Bq = J->Bf + (int64_t)q * kb * N + c0;
+      for (int64_t i = 0; i < rb * n; ++i) gf[i] = 0.0f;
+      for (int64_t t = 0; t < kb; ++t) {
+        const float* brow = Bq + t * N;
+        for (int64_t r = 0; r < rb; ++r) {
+          const float a = (float)Ap[(r0 + r) * kb + t];
+          if (a == 0.0f) continue; /* +-0 products never change g: g starts at +0, RNE sums never give -0 */
+          float* g = gf + r * n;
+          for (int64_t j = 0; j < n; ++j) g[j] = g[j] + a * brow[j];
+        }
+      }
+    } else {
+      const double* Bq = J->coeffB + (int64_t)q * kb * N + c0;
+      for (int64_t i = 0; i < rb * n; ++i) gd[i] = 0.0;
+      for (int64_t t = 0; t < kb; ++t) {
+        const double* brow = Bq + t * N;
+        for (int64_t r = 0; r < rb; ++r) {
+          const double a = Ap[(r0 + r) * kb + t];
+          if (a == 0.0) continue;
+          double* g = gd + r * n;
+          for (int64_t j = 0; j < n; ++j) g[j] = g[j] + a * brow[j];
+        }
+      }
+    }
+    for (int64_t r = 0; r < rb; ++r) {
+      const int64_t ea = J->expoA[(int64_t)p * m + r0 + r];
+      for (int64_t j = 0; j < n; ++j) {
+        const double g = J->fp32 ? (double)gf[r * n + j] : gd[r * n + j];
+        const uint64_t tb = scale_term(g, ea + J->expoB[(int64_t)q * N + c0 + j], J->emu, flags);
+        double* cb = Cb + r * n + j;
+        if (J->emu) *cb = dbl(oro_emu_add(bits(*cb), tb, flags));
+        else *cb = *cb + dbl(tb);
+      }
+    }
+  }
+  for (int64_t r = 0; r < rb; ++r)
+    for (int64_t j = 0; j < n; ++j) {
+      double* c = J->C + (r0 + r) * N + c0 + j;
+      const double v = Cb[r * n + j];
+      if (!J->accumulate) *c = J->emu ? dbl(oro_emu_add(0, bits(v), flags)) : 0.0 + v;
+      else *c = J->emu ? dbl(oro_emu_add(bits(*c), bits(v), flags)) : *c + v;
+    }
+}
+
+static void* block_worker(void* arg) {
+  BlockJob* J = (BlockJob*)arg;
+  double* Cb = (double*)malloc(sizeof(double) * RB * CB + 8);
+  float* gf = (float*)malloc(sizeof(float) * RB * CB + 8);
+  double* gd = (double*)malloc(sizeof(double) * RB * CB + 8);
+  uint32_t flags = 0;
+  const int64_t ncb = (J->n + CB - 1) / CB, nblocks = ((J->m + RB - 1) / RB) * ncb;
+  for (;;) {
+    pthread_mutex_lock(&J->mu);
+    const int64_t b = J->next_block++;
+    pthread_mutex_unlock(&J->mu);
+    if (b >= nblocks) break;
+    block_rows(J, (b / ncb) * RB, (b % ncb) * CB, Cb, gf, gd, &flags);
+  }
+  pthread_mutex_lock(&J->mu);
+  J->flags |= flags;
+  pthread_mutex_unlock(&J->mu);
+  free(Cb); free(gf); free(gd);
+  return NULL;
+}
+
+void oro_pair_block(const double* coeffA, const int32_t* expoA, const double* coeffB, const int32_t* expoB,
+                    int64_t m, int64_t n, int64_t kb, int sx, int sy, int order, int cutoff, int emu, int fp32,
+                    int accumulate, double* C, int nthreads, uint32_t* flags_out) {
+  BlockJob J;
+  memset(&J, 0, sizeof J);
+  int* pp = (int*)malloc(sizeof(int) * (sx * sy + 1));
+  int* qq = (int*)malloc(sizeof(int) * (sx * sy + 1));
+  float* Bf = NULL;
+  if (fp32) { /* B planes as float (exact: slice values fit in fp32) */
+    Bf = (float*)malloc(sizeof(float) * (size_t)sy * kb * n + 4);
+    for (int64_t i = 0; i < (int64_t)sy * kb * n; ++i) Bf[i] = (float)coeffB[i];
+  }
+  J.coeffA = coeffA; J.expoA = expoA; J.coeffB = coeffB; J.Bf = Bf; J.expoB = expoB;
+  J.m = m; J.n = n; J.kb = kb; J.pp = pp; J.qq = qq; J.np = build_pairs(sx, sy, order, cutoff, pp, qq);
+  J.emu = emu; J.fp32 = fp32; J.accumulate = accumulate; J.C = C;
+  pthread_mutex_init(&J.mu, NULL);
+  if (nthreads < 1) nthreads = 1;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * nthreads);
+  for (int i = 1; i < nthreads; ++i) pthread_create(&th[i], NULL, block_worker, &J);
+  block_worker(&J);
+  for (int i = 1; i < nthreads; ++i) pthread_join(th[i], NULL);
+  pthread_mutex_destroy(&J.mu);
+  *flags_out |= J.flags;
+  free(th); free(Bf); free(pp); free(qq);
+}
+
+int oro_max_threads(void) {
+  const long n = sysconf(_SC_NPROCESSORS_ONLN);
+  return n > 0 ? (int)n : 1;
+}

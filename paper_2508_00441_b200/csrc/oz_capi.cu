@@ -1,0 +1,251 @@
+// oz_capi.cu — the C ABI of liboz_b200.so (declared in include/oz_b200.h).
+// Unity build: the kernel translation units are included here so one nvcc
+// invocation produces the whole library.
+#include "oz_tile_gemm.cu"
+#include "oz_pair_gemm.cu"
+#include "oz_split.cu"
+#include "oz_dd_gemm.cu"
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/oz_b200.h"
+
+namespace {
+
+using oz::LpFormat;
+
+bool fmt_info(int type2, LpFormat& f, uint32_t& idesc_fmt) {
+  switch (type2) {
+    case OZ_FMT_E4M3: f = {4, 3, 7, 15, 1, 1}; idesc_fmt = 0; return true;
+    case OZ_FMT_E5M2: f = {5, 2, 15, 30, 0, 1}; idesc_fmt = 1; return true;
+    case OZ_FMT_FP16: f = {5, 10, 15, 30, 0, 2}; idesc_fmt = 0; return true;
+    case OZ_FMT_BF16: f = {8, 7, 127, 254, 0, 2}; idesc_fmt = 1; return true;
+    default: return false;
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 3-D map over slice planes [planes][rows][ld] with a 128-byte x 128-row box, SWIZZLE_128B.
+int make_plane_map(CUtensorMap* map, const void* base, int elem_bytes, int64_t k, int64_t rows, int64_t planes,
+                   int64_t ld) {
+  EncodeFn enc = get_encode();
+  if (!enc) return OZ_ETMAP;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * elem_bytes) & 15)) return OZ_EINVAL;
+  const cuuint64_t dims[3] = {(cuuint64_t)k, (cuuint64_t)rows, (cuuint64_t)planes};
+  const cuuint64_t strides[2] = {(cuuint64_t)(ld * elem_bytes), (cuuint64_t)(ld * elem_bytes * rows)};
+  const cuuint32_t box[3] = {(cuuint32_t)(128 / elem_bytes), 128u, 1u};
+  const cuuint32_t estr[3] = {1u, 1u, 1u};
+  const CUresult r =
+      enc(map, elem_bytes == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3,
+          const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? OZ_OK : OZ_ETMAP;
+}
+
+int num_sms() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+int launch_status() {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "oz_b200: CUDA launch error: %s\n", cudaGetErrorString(e));
+    return OZ_ECUDA;
+  }
+  return OZ_OK;
+}
+
+template <bool kWrite>
+int launch_split(const oz::SplitParams& P, int emu, cudaStream_t st) {
+  const int64_t need = (P.ld > P.kb ? P.ld : P.kb);
+  int ept;
+  if (need <= 256 * 4) ept = 4;
+  else if (need <= 256 * 8) ept = 8;
+  else if (need <= 256 * 16) ept = 16;
+  else if (need <= 256 * 32) ept = 32;
+  else if (need <= 256 * 64) ept = 64;
+  else return OZ_EUNSUPPORTED;  // kb > 16384: needs the cluster split (not yet built)
+  const dim3 grid((unsigned)P.rows), block(oz::kSplitThreads);
+#define OZ_SPLIT_CASE(E)                                                              \
+  case E:                                                                             \
+    if (emu) oz::split_rows_kernel<E, kWrite, true><<<grid, block, 0, st>>>(P);       \
+    else oz::split_rows_kernel<E, kWrite, false><<<grid, block, 0, st>>>(P);          \
+    break;
+  switch (ept) {
+    OZ_SPLIT_CASE(4)
+    OZ_SPLIT_CASE(8)
+    OZ_SPLIT_CASE(16)
+    OZ_SPLIT_CASE(32)
+    OZ_SPLIT_CASE(64)
+  }
+#undef OZ_SPLIT_CASE
+  return launch_status();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* oz_version(void) { return "oz_b200 0.1 (sm_100a tcgen05; reference ozdgemm 1.0.0 semantics)"; }
+
+const char* oz_strerror(int status) {
+  switch (status) {
+    case OZ_OK: return "ok";
+    case OZ_EINVAL: return "invalid argument";
+    case OZ_EUNSUPPORTED: return "unsupported format or size on sm_100a";
+    case OZ_ECUDA: return "CUDA launch error";
+    case OZ_ETMAP: return "cuTensorMapEncodeTiled failed";
+    case OZ_ESLICES: return "too many B slices for the fused epilogue (max 64)";
+    default: return "unknown status";
+  }
+}
+
+int oz_split_count(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2, int rho, int emu,
+                   int32_t* row_cnt, int32_t* s_max, uint32_t* flags, void* stream) {
+  oz::SplitParams P{};
+  uint32_t idf;
+  if (!fmt_info(type2, P.fmt, idf)) return OZ_EUNSUPPORTED;
+  if (rows < 0 || kb < 1 || ldx < kb || !X || !row_cnt || !s_max || !flags) return OZ_EINVAL;
+  if (rows == 0) return OZ_OK;
+  P.X = X; P.rows = rows; P.kb = kb; P.ldx = ldx; P.rho = rho;
+  P.planes = 0; P.coeff = nullptr; P.ld = kb; P.expo = nullptr;
+  P.row_cnt = row_cnt; P.s_max = s_max; P.flags = flags;
+  return launch_split<false>(P, emu, (cudaStream_t)stream);
+}
+
+int oz_split_rows(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2, int rho, int emu, int planes,
+                  void* coeff, int64_t ld_coeff, int32_t* expo, int32_t* row_cnt, uint32_t* flags, void* stream) {
+  oz::SplitParams P{};
+  uint32_t idf;
+  if (!fmt_info(type2, P.fmt, idf)) return OZ_EUNSUPPORTED;
+  if (rows < 0 || kb < 1 || ldx < kb || ld_coeff < kb || planes < 0 || !X || !row_cnt || !flags) return OZ_EINVAL;
+  if ((ld_coeff * P.fmt.bytes) % 16) return OZ_EINVAL;
+  if (rows == 0 || planes == 0) return OZ_OK;
+  if (!coeff || !expo) return OZ_EINVAL;
+  P.X = X; P.rows = rows; P.kb = kb; P.ldx = ldx; P.rho = rho;
+  P.planes = planes; P.coeff = static_cast<uint8_t*>(coeff); P.ld = ld_coeff; P.expo = expo;
+  P.row_cnt = row_cnt; P.s_max = nullptr; P.flags = flags;
+  return launch_split<true>(P, emu, (cudaStream_t)stream);
+}
+
+int oz_transpose(const double* src, int64_t rows, int64_t cols, int64_t ld_src, double* dst, int64_t ld_dst,
+                 void* stream) {
+  if (rows < 0 || cols < 0 || ld_src < cols || ld_dst < rows) return OZ_EINVAL;
+  if (rows == 0 || cols == 0) return OZ_OK;
+  if (!src || !dst) return OZ_EINVAL;
+  const dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  oz::transpose_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(src, rows, cols, ld_src, dst, ld_dst);
+  return launch_status();
+}
+
+int oz_tile_counts(const int32_t* row_cnt, int64_t rows, int32_t* tile_cnt, void* stream) {
+  if (rows < 0 || !row_cnt || !tile_cnt) return OZ_EINVAL;
+  if (rows == 0) return OZ_OK;
+  oz::tile_counts_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, (cudaStream_t)stream>>>(row_cnt, rows, tile_cnt);
+  return launch_status();
+}
+
+int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64_t ld_b, int planes_a,
+                 int planes_b, const int32_t* expo_a, const int32_t* expo_b, const int32_t* tile_cnt_a,
+                 const int32_t* tile_cnt_b, int64_t m, int64_t n, int64_t kb, int sx, int sy, int type2,
+                 int order, int pair_cutoff, int emu, int accumulate, double* C, int64_t ldc, uint32_t* flags,
+                 void* stream) {
+  LpFormat f;
+  uint32_t idf;
+  if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
+  if (m < 0 || n < 0 || kb < 1 || sx < 0 || sy < 0 || sx > planes_a || sy > planes_b || ldc < n || !C || !flags)
+    return OZ_EINVAL;
+  if ((tile_cnt_a == nullptr) != (tile_cnt_b == nullptr)) return OZ_EINVAL;
+  if (sy > oz::kMaxSy) return OZ_ESLICES;
+  if (m == 0 || n == 0) return OZ_OK;
+  if (m > INT32_MAX || n > INT32_MAX || kb > INT32_MAX) return OZ_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (sx == 0 || sy == 0) {
+    // No pairs at all: Cb = 0, so C = 0 (first block) or C unchanged.
+    if (!accumulate) {
+      if (ldc == n) cudaMemsetAsync(C, 0, sizeof(double) * m * n, st);
+      else cudaMemset2DAsync(C, ldc * sizeof(double), 0, n * sizeof(double), m, st);
+    }
+    return launch_status();
+  }
+  if (!a_planes || !b_planes || !expo_a || !expo_b) return OZ_EINVAL;
+  CUtensorMap ma, mb;
+  int rc = make_plane_map(&ma, a_planes, f.bytes, kb, m, planes_a, ld_a);
+  if (rc) return rc;
+  rc = make_plane_map(&mb, b_planes, f.bytes, kb, n, planes_b, ld_b);
+  if (rc) return rc;
+  oz::PairParams P{};
+  P.expo_a = expo_a; P.expo_b = expo_b; P.tile_cnt_a = tile_cnt_a; P.tile_cnt_b = tile_cnt_b;
+  P.C = C; P.ldc = ldc; P.m = (int)m; P.n = (int)n; P.kb = (int)kb; P.sx = sx; P.sy = sy;
+  P.order = order; P.cutoff = pair_cutoff; P.accumulate = accumulate;
+  P.tiles_m = (int)((m + oz::kPM - 1) / oz::kPM); P.tiles_n = (int)((n + oz::kPN - 1) / oz::kPN);
+  P.elem_bytes = f.bytes; P.fmt = idf; P.flags = flags;
+  const size_t smem = oz::pair_gemm_smem_bytes();
+  const int tiles = P.tiles_m * P.tiles_n;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  if (emu) {
+    cudaFuncSetAttribute(oz::pair_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    oz::pair_gemm_kernel<true><<<grid, oz::kPThreads, smem, st>>>(ma, mb, P);
+  } else {
+    cudaFuncSetAttribute(oz::pair_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    oz::pair_gemm_kernel<false><<<grid, oz::kPThreads, smem, st>>>(ma, mb, P);
+  }
+  return launch_status();
+}
+
+int oz_dd_gemm(const double* A, const double* B, double* C, int64_t m, int64_t n, int64_t k, void* stream) {
+  if (m < 0 || n < 0 || k < 0 || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) return OZ_EINVAL;
+  if (m == 0 || n == 0) return OZ_OK;
+  if (!A || !B || !C) return OZ_EINVAL;
+  const dim3 grid((unsigned)((n + 63) / 64), (unsigned)((m + 63) / 64));
+  oz::dd_gemm_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(A, B, C, (int)m, (int)n, (int)k);
+  return launch_status();
+}
+
+int oz_lp_gemm(const void* a_plane, const void* b_plane, int64_t ld_a, int64_t ld_b, int64_t m, int64_t n,
+               int64_t k, int type2, float* D, int64_t ldd, void* stream) {
+  LpFormat f;
+  uint32_t idf;
+  if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
+  if (m < 0 || n < 0 || k < 0 || ldd < n || !D) return OZ_EINVAL;
+  if (m == 0 || n == 0) return OZ_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k == 0) {
+    cudaMemset2DAsync(D, ldd * sizeof(float), 0, n * sizeof(float), m, st);
+    return launch_status();
+  }
+  if (!a_plane || !b_plane || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) return OZ_EINVAL;
+  CUtensorMap ma, mb;
+  int rc = make_plane_map(&ma, a_plane, f.bytes, k, m, 1, ld_a);
+  if (rc) return rc;
+  rc = make_plane_map(&mb, b_plane, f.bytes, k, n, 1, ld_b);
+  if (rc) return rc;
+  const size_t smem = oz::tile_gemm_smem_bytes();
+  cudaFuncSetAttribute(oz::tile_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const dim3 grid((unsigned)((m + oz::kTileM - 1) / oz::kTileM), (unsigned)((n + oz::kTileN - 1) / oz::kTileN));
+  oz::tile_gemm_kernel<<<grid, 128, smem, st>>>(ma, mb, D, ldd, (int)m, (int)n, (int)k, 0, 0, f.bytes, idf);
+  return launch_status();
+}
+
+}  // extern "C"

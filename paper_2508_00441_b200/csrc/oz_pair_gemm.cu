@@ -1,0 +1,354 @@
+// oz_pair_gemm.cu — K3: fused slice-pair GEMM + exact scaling + ordered FP64 accumulation.
+//
+// Replaces, for one inner-product block, the reference's pair loop
+//   ozgemm.py:179-183   pair list sorted by (-(p+q), p, q)  (or (p+q, p, q))
+//   ozgemm.py:188-190   G = lp_gemm(A_p, B_q)              (error-free product)
+//   ozgemm.py:192-193   T = ldexp(G, cA_p[i] + cB_q[j])     (_scale_terms_exact :132-140)
+//   ozgemm.py:194-197   Cb = Cb + T   (hardware FP64 or fp64emu.add_arrays)
+//   ozgemm.py:204-207   C  = C + Cb   (ascending blocks)
+// G never touches HBM.  Per 128 x 128 output tile (one CTA, persistent):
+//   warp 0      TMA producer: A_p / B_q k-blocks (128 B rows, SWIZZLE_128B) into a
+//               kStages-deep smem ring;
+//   warp 1      tcgen05.mma issuer (kind::f8f6f4 E4M3/E5M2 or kind::f16 F16/BF16,
+//               FP32 accumulate) into one of kAccBufs TMEM accumulators per pair;
+//               owns the TMEM allocation;
+//   warps 4..11 epilogue (setmaxnreg 232; warps 2-3 idle at 40 regs): tcgen05.ld the FP32 G, rebuild T = G * 2^(eA+eB) as an
+//               FP64 bit pattern with integer ops (exact), and add it into the
+//               register-resident FP64 Cb in the reference pair order, with
+//               __dadd_rn (HW mode) or the integer-only emu_add (EMU mode — this
+//               instantiation contains no DADD/DMUL/DFMA, see tests/test_sass.py).
+// Pairs whose A- or B-slice is all-zero over the tile (per-tile slice counts)
+// may be skipped: the term is +0 and Cb is never -0, so the result is unchanged.
+#include <type_traits>
+
+#include "oz_common.cuh"
+
+namespace oz {
+
+constexpr int kPM = 128, kPN = 128;        // output tile
+constexpr int kPStages = 5;                // smem ring depth
+constexpr int kPStageBytes = 2 * 128 * 128;
+constexpr int kAccBufs = 4;                // TMEM accumulators (4 x 128 cols = 512)
+constexpr int kEpiWarps = 8;
+constexpr int kPThreads = 128 + 32 * kEpiWarps;  // WG0: TMA, MMA, 2 idle; WG1-2: epilogue
+constexpr int kMaxSy = 64;                 // B-exponent staging cap (planes)
+
+struct PairSmem {
+  alignas(1024) uint8_t a[kPStages][128 * 128];
+  alignas(1024) uint8_t b[kPStages][128 * 128];
+  int32_t eb[kMaxSy][kPN];
+  uint64_t full[kPStages], empty[kPStages];
+  uint64_t acc_full[kAccBufs], acc_empty[kAccBufs];
+  uint32_t tmem_base;
+};
+
+struct PairParams {
+  const int32_t* expo_a;     // [sx_planes][m]
+  const int32_t* expo_b;     // [sy_planes][n]
+  const int32_t* tile_cnt_a; // [tiles_m] max slice count over the tile's rows (nullable = no skip)
+  const int32_t* tile_cnt_b; // [tiles_n]
+  double* C;
+  int64_t ldc;
+  int m, n, kb;
+  int sx, sy;                // slice counts after max_slices
+  int order;                 // 0 = smallest-first, 1 = largest-first
+  int cutoff;                // keep pairs with p+q <= cutoff  (< 0: keep all)
+  int accumulate;            // 0: C = Cb (first block), 1: C = C + Cb
+  int tiles_m, tiles_n;
+  int elem_bytes;            // 1: kind::f8f6f4, 2: kind::f16
+  uint32_t fmt;              // idesc a/b format code
+  uint32_t* flags;
+};
+
+// Pair enumeration in reference order restricted to p < lp, q < lq, p+q <= cut.
+struct PairIter {
+  int lp, lq, dmax, d, p, dir;
+  OZ_DEVICE void init(int lp_, int lq_, int order, int cutoff) {
+    lp = lp_;
+    lq = lq_;
+    dmax = lp + lq - 2;
+    if (cutoff >= 0 && cutoff < dmax) dmax = cutoff;
+    dir = order == 0 ? -1 : 1;
+    d = order == 0 ? dmax : 0;
+    p = 0;
+    if (lp <= 0 || lq <= 0) {
+      d = -1;
+      dir = -1;
+      return;
+    }
+    p = d - (lq - 1) > 0 ? d - (lq - 1) : 0;
+  }
+  OZ_DEVICE bool valid() const { return d >= 0 && d <= dmax; }
+  OZ_DEVICE int q() const { return d - p; }
+  OZ_DEVICE void next() {
+    const int pend = d < lp - 1 ? d : lp - 1;
+    if (p < pend) {
+      ++p;
+      return;
+    }
+    d += dir;
+    if (valid()) p = d - (lq - 1) > 0 ? d - (lq - 1) : 0;
+  }
+};
+
+OZ_DEVICE void tile_coords(int tile, int tiles_m, int tiles_n, int& tm, int& tn) {
+  // Grouped raster: bands of 16 row-tiles walk across the column tiles, so the
+  // CTAs resident at one time share A and B k-panels in L2.
+  constexpr int G = 16;
+  const int band = tile / (G * tiles_n);
+  const int first_m = band * G;
+  const int gm = min(G, tiles_m - first_m);
+  const int r = tile - band * G * tiles_n;
+  tm = first_m + r % gm;
+  tn = r / gm;
+}
+
+OZ_DEVICE void tile_limits(const PairParams& P, int tm, int tn, int& lp, int& lq) {
+  lp = P.sx;
+  lq = P.sy;
+  if (P.tile_cnt_a) {
+    lp = min(lp, __ldg(P.tile_cnt_a + tm));
+    lq = min(lq, __ldg(P.tile_cnt_b + tn));
+  }
+}
+
+// T = ldexp(G, e) rebuilt from the FP32 bit pattern of a non-zero G (always a
+// normal FP32: a non-zero multiple of 2^(2(rho-53)) below 2^24).  Returns false
+// (and sets *zero) when the exact term underflows the reference's way.
+OZ_DEVICE bool make_term(uint32_t g, int e, uint64_t& t, uint32_t& flags, bool emu) {
+  const int ex = (int)((g >> 23) & 0xFFu) + (1023 - 127) + e;
+  const uint64_t sign = (uint64_t)(g >> 31) << 63;
+  const uint64_t frac = (uint64_t)(g & 0x7FFFFFu) << 29;
+  if ((unsigned)(ex - 1) < 2046u) {
+    t = sign | ((uint64_t)ex << 52) | frac;
+    return true;
+  }
+  // Out of the normal range: overflow is always an error; in HW mode a total
+  // underflow rounds to +-0 silently (np.ldexp, ozgemm.py:136-139), a subnormal
+  // result is an error.  The emulated scale2 rejects both (fp64emu.py:269-277).
+  if (emu || ex > 2046) {
+    flags |= FLAG_TERM_RANGE;
+    return false;
+  }
+  const int lead = ex - 1023;  // exponent of the leading bit
+  if (lead <= -1076 || (lead == -1075 && frac == 0)) return false;  // rounds to zero
+  flags |= FLAG_TERM_RANGE;
+  return false;
+}
+
+template <bool kEmu>
+__global__ void __launch_bounds__(kPThreads, 1)
+    pair_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                     const PairParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  PairSmem& s = *reinterpret_cast<PairSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x / 32;
+  const int lane = (int)lane_id();
+  const int num_tiles = P.tiles_m * P.tiles_n;
+  const int kb_elems = 128 / P.elem_bytes;
+  const int num_kb = (P.kb + kb_elems - 1) / kb_elems;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int i = 0; i < kPStages; ++i) {
+      mbar_init(&s.full[i], 1);
+      mbar_init(&s.empty[i], 1);
+    }
+    for (int i = 0; i < kAccBufs; ++i) {
+      mbar_init(&s.acc_full[i], 1);
+      mbar_init(&s.acc_empty[i], kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<kAccBufs * kPN>(&s.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+  if (warp == 0) {
+    // ───────── TMA producer ─────────
+    if (elect_one()) {
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int tm, tn, lp, lq;
+        tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
+        tile_limits(P, tm, tn, lp, lq);
+        PairIter pi;
+        for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next()) {
+          const int p = pi.p, q = pi.q();
+          for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
+            const uint32_t st = it % kPStages;
+            if (it >= (uint32_t)kPStages) mbar_wait(&s.empty[st], ((it / kPStages) - 1) & 1);
+            mbar_arrive_expect_tx(&s.full[st], kPStageBytes);
+            tma_load_3d(s.a[st], &map_a, &s.full[st], kbi * kb_elems, tm * kPM, p, kEvictNormal);
+            tma_load_3d(s.b[st], &map_b, &s.full[st], kbi * kb_elems, tn * kPN, q, kEvictNormal);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ───────── MMA issuer ─────────
+    const uint32_t idesc = make_idesc(P.fmt, P.fmt, kPM, kPN);
+    uint32_t it = 0, acc_it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      int tm, tn, lp, lq;
+      tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
+      tile_limits(P, tm, tn, lp, lq);
+      PairIter pi;
+      for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
+        const uint32_t buf = acc_it % kAccBufs;
+        if (acc_it >= (uint32_t)kAccBufs) mbar_wait(&s.acc_empty[buf], ((acc_it / kAccBufs) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + buf * kPN;
+        for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
+          const uint32_t st = it % kPStages;
+          mbar_wait(&s.full[st], (it / kPStages) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t ad = smem_desc_sw128(s.a[st]), bd = smem_desc_sw128(s.b[st]);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t off = (uint64_t)((kk * 32) >> 4);
+              if (P.elem_bytes == 1)
+                mma_f8f6f4(d_tmem, ad + off, bd + off, idesc, (kbi | kk) != 0);
+              else
+                mma_f16(d_tmem, ad + off, bd + off, idesc, (kbi | kk) != 0);
+            }
+            mma_commit(&s.empty[st]);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) mma_commit(&s.acc_full[buf]);
+        __syncwarp();
+      }
+    }
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+    // ───────── epilogue: ordered FP64 accumulation ─────────
+    const int quad = warp & 3;               // TMEM lane quadrant this warp may access
+    const int half = (warp - 4) >> 2;        // column half [64*half, 64*half+64)
+    const int epi_tid = threadIdx.x - 128;   // 0..255
+    uint32_t flags = 0;
+    uint32_t acc_it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      int tm, tn, lp, lq;
+      tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
+      tile_limits(P, tm, tn, lp, lq);
+      const int row = tm * kPM + quad * 32 + lane;
+      const int col0 = tn * kPN + half * 64;
+      // Stage the tile's B exponents (all planes we will touch) in smem.
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      for (int idx = epi_tid; idx < lq * kPN; idx += 32 * kEpiWarps) {
+        const int q = idx / kPN, c = idx % kPN, gc = tn * kPN + c;
+        s.eb[q][c] = gc < P.n ? __ldg(P.expo_b + (int64_t)q * P.n + gc) : 0;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+
+      // Emulated mode keeps Cb as raw bit patterns: no double-typed value may
+      // exist, or nvcc turns bit tricks into FP64 instructions (e.g. DADD |x|).
+      using Acc = typename std::conditional<kEmu, uint64_t, double>::type;
+      Acc cb[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) cb[j] = Acc(0);
+
+      PairIter pi;
+      for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
+        const int p = pi.p, q = pi.q();
+        const int ea = row < P.m ? __ldg(P.expo_a + (int64_t)p * P.m + row) : 0;
+        const uint32_t buf = acc_it % kAccBufs;
+        mbar_wait(&s.acc_full[buf], (acc_it / kAccBufs) & 1);
+        tc_fence_after();
+        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + buf * kPN + half * 64;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t g[16];
+          tmem_ld16(taddr + ch * 16, g);
+          tmem_ld_wait();
+          const int4* ebv = reinterpret_cast<const int4*>(&s.eb[q][half * 64 + ch * 16]);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int4 e4 = ebv[v];
+            const int eb4[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int j = ch * 16 + v * 4 + u;
+              const uint32_t gv = g[v * 4 + u];
+              if ((gv << 1) != 0u) {
+                uint64_t t;
+                if (make_term(gv, ea + eb4[u], t, flags, kEmu)) {
+                  if constexpr (kEmu)
+                    cb[j] = emu_add(cb[j], t, flags);
+                  else
+                    cb[j] = __dadd_rn(cb[j], u2d(t));
+                }
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s.acc_empty[buf]);
+      }
+
+      // C = Cb (first block) or C = C + Cb (ozgemm.py:204-207).
+      if (row < P.m) {
+        Acc* crow = reinterpret_cast<Acc*>(P.C + (int64_t)row * P.ldc + col0);
+        const bool vec = ((P.ldc & 1) == 0) && (col0 + 64 <= P.n);
+        if (vec) {
+          using Acc2 = typename std::conditional<kEmu, ulonglong2, double2>::type;
+#pragma unroll
+          for (int j = 0; j < 64; j += 2) {
+            Acc2 v;
+            if (P.accumulate) {
+              const Acc2 c = *reinterpret_cast<const Acc2*>(crow + j);
+              if constexpr (kEmu) {
+                v.x = emu_add(c.x, cb[j], flags);
+                v.y = emu_add(c.y, cb[j + 1], flags);
+              } else {
+                v.x = __dadd_rn(c.x, cb[j]);
+                v.y = __dadd_rn(c.y, cb[j + 1]);
+              }
+            } else {
+              v.x = cb[j];
+              v.y = cb[j + 1];
+            }
+            *reinterpret_cast<Acc2*>(crow + j) = v;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 64; ++j) {
+            if (col0 + j < P.n) {
+              Acc v = cb[j];
+              if (P.accumulate) {
+                if constexpr (kEmu)
+                  v = emu_add(crow[j], cb[j], flags);
+                else
+                  v = __dadd_rn(crow[j], cb[j]);
+              }
+              crow[j] = v;
+            }
+          }
+        }
+      }
+    }
+    if (flags) atomicOr(P.flags, flags);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<kAccBufs * kPN>(tmem);
+}
+
+template __global__ void pair_gemm_kernel<false>(const __grid_constant__ CUtensorMap,
+                                                 const __grid_constant__ CUtensorMap, const PairParams);
+template __global__ void pair_gemm_kernel<true>(const __grid_constant__ CUtensorMap,
+                                                const __grid_constant__ CUtensorMap, const PairParams);
+
+size_t pair_gemm_smem_bytes() { return sizeof(PairSmem) + 1024; }
+
+}  // namespace oz

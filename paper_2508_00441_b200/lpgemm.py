@@ -1,0 +1,108 @@
+"""One slice-pair product on the tensor cores — the ``lp_gemm`` seam.
+
+The reference simulates a low-precision GEMM with per-step RNE accumulation
+in numpy (lpgemm.py:93-120).  Here the operands are real FP8/FP16 codes fed
+to one tcgen05 MMA tile kernel (``oz_lp_gemm``) with FP32 accumulation in
+TMEM.  For slice operands the product is exact (error-free by construction),
+so the result equals the reference's bit for bit; that is the only regime the
+pipeline uses.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .errors import RepresentabilityError
+from .formats import FormatSpec, decode_codes
+
+__all__ = ["RepresentabilityError", "LpMatrix", "lp_gemm", "encode_values"]
+
+
+class LpMatrix:
+    """Matrix whose entries are representable in ``fmt`` (lpgemm.py:27-46)."""
+
+    def __init__(self, data, fmt: FormatSpec, _validated: bool = False):
+        self.data = np.asarray(data, dtype=np.float64)
+        self.fmt = fmt
+        if self.data.ndim != 2:
+            raise ValueError("LpMatrix expects a 2-D matrix")
+        if not _validated:
+            encode_values(self.data, fmt)  # raises RepresentabilityError
+
+    @property
+    def shape(self):
+        return self.data.shape
+
+
+def encode_values(vals: np.ndarray, fmt: FormatSpec) -> np.ndarray:
+    """Exact float64 values -> storage codes (uint8 / uint16); raises
+    RepresentabilityError for a value the format cannot hold exactly."""
+    vals = np.asarray(vals, dtype=np.float64)
+    if fmt.name in ("fp8e4m3", "fp8e5m2"):
+        table = decode_codes(np.arange(256, dtype=np.uint8), fmt.name)
+        ok = np.isfinite(table)
+        if fmt.name == "fp8e4m3":
+            ok &= np.arange(256) & 0x7F != 0x7F  # S.1111.111 is NaN
+        else:
+            ok &= (np.arange(256) >> 2) & 0x1F != 0x1F
+        codes_ok = np.nonzero(ok)[0]
+        vals_ok = table[codes_ok]
+        order = np.argsort(vals_ok, kind="stable")
+        sv, sc = vals_ok[order], codes_ok[order]
+        idx = np.clip(np.searchsorted(sv, vals), 0, sv.size - 1)
+        if not np.all(sv[idx] == vals):
+            raise RepresentabilityError(f"matrix entries not representable in {fmt.name}")
+        out = sc[idx].astype(np.uint8)
+        out[vals == 0] = 0
+        return out
+    if fmt.name == "fp16":
+        h = vals.astype(np.float16)
+        if not np.array_equal(h.astype(np.float64), vals):
+            raise RepresentabilityError(f"matrix entries not representable in {fmt.name}")
+        return h.view(np.uint16)
+    if fmt.name == "bf16":
+        f = vals.astype(np.float32)
+        bits = f.view(np.uint32)
+        if not np.array_equal(f.astype(np.float64), vals) or np.any(bits & 0xFFFF):
+            raise RepresentabilityError(f"matrix entries not representable in {fmt.name}")
+        return (bits >> 16).astype(np.uint16)
+    raise NotImplementedError(f"no tensor-core operand path for {fmt.name} in this build")
+
+
+def _padded_codes(torch, codes: np.ndarray):
+    rows, k = codes.shape
+    per16 = 16 // codes.itemsize
+    ld = -(-max(k, 1) // per16) * per16
+    buf = np.zeros((rows, ld), dtype=codes.dtype)
+    buf[:, :k] = codes
+    t = torch.from_numpy(buf.view(np.uint8) if codes.itemsize == 1 else buf.view(np.int16)).cuda()
+    return t, ld
+
+
+def lp_gemm(A: LpMatrix, B: LpMatrix, type3: FormatSpec) -> np.ndarray:
+    """C = A @ B with FP32 tensor-core accumulation (exact on slice operands)."""
+    if A.shape[1] != B.shape[0]:
+        raise ValueError("inner dimensions do not match")
+    if 2 * max(A.fmt.mant_bits, B.fmt.mant_bits) > 53:
+        raise AssertionError("operand products would not be exact in FP64")
+    if A.fmt.name != B.fmt.name:
+        raise NotImplementedError("mixed operand formats are not wired to tcgen05 in this build")
+    if type3.mant_bits > 24:
+        raise NotImplementedError("accumulators wider than FP32 are not available on the tensor cores")
+    torch = _lib.require_cuda()
+    m, k = A.shape
+    n = B.shape[1]
+    if k == 0 or m == 0 or n == 0:
+        return np.zeros((m, n))
+    ca = encode_values(A.data, A.fmt)
+    cb = encode_values(np.ascontiguousarray(B.data.T), B.fmt)  # K-major B
+    ta, lda = _padded_codes(torch, ca)
+    tb, ldb = _padded_codes(torch, cb)
+    D = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    _lib.call("oz_lp_gemm", ta.data_ptr(), tb.data_ptr(), lda, ldb, m, n, k, _lib.FMT_CODE[A.fmt.name],
+              D.data_ptr(), n, _lib.stream_ptr(torch))
+    out = D.double().cpu().numpy()
+    if not np.all(np.isfinite(out)):
+        raise OverflowError("accumulation overflowed fp32")
+    return out

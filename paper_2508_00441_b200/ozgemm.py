@@ -1,0 +1,243 @@
+"""FP64 GEMM from FP8/FP16 tensor-core slice products — B200 pipeline.
+
+Drop-in for ``ozdgemm.ozgemm`` (ozgemm.py:47-224): same ``GemmConfig`` fields
+and validation, same ``OzStats``/``OzResult`` schema, same block loop and pair
+order, bitwise the same C.  Per inner-product block [lo, hi)
+(ozgemm.py:160-209):
+
+  split A[:, lo:hi] by rows, B[lo:hi, :] by columns   -> oz_split.cu   (HBM-bound)
+  all slice pairs, reference order, G exact in TMEM,
+  T = G*2^(eA+eB) and Cb += T in the epilogue,
+  C = Cb (first block) / C + Cb                        -> oz_pair_gemm.cu (tensor-bound)
+
+Two opt-in extensions beyond the reference, both off by default:
+  * ``pair_cutoff = d`` keeps only pairs with p + q <= d (a prefix-free subset
+    of the reference order; ``d >= sx + sy - 2`` is exactly the reference);
+  * ``skip_zero_pairs`` (default on) skips pairs whose A- or B-slice is all zero
+    over a 128x128 output tile: such a term is +0 and Cb is never -0, so C is
+    bitwise unchanged (this is not an approximation).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import DimensionError, SlicingInfeasible
+from .formats import FormatSpec
+from .slicing import compute_params, predict_gemm_count, split_rows_device, transpose_device
+
+__all__ = [
+    "DimensionError", "GemmConfig", "BlockStats", "OzStats", "OzResult", "transpose", "oz_gemm",
+    "oz_gemm_count", "oz_gemm_device", "pair_order",
+]
+
+_ACC_ORDERS = ("smallest-first", "largest-first")
+
+
+@dataclass(frozen=True)
+class GemmConfig:
+    """Options of one emulated DGEMM (ozgemm.py:47-73) plus B200 extensions."""
+
+    type2: FormatSpec
+    type3: FormatSpec
+    k_block: int = 0
+    fp64_emulation: bool = False
+    max_slices: int | None = None
+    accumulation_order: str = "smallest-first"
+    seed: int = 0
+    # ---- extensions (defaults reproduce the reference bit for bit) ----
+    pair_cutoff: int | None = None
+    skip_zero_pairs: bool = True
+
+    def __post_init__(self):
+        if self.k_block < 0:
+            raise ValueError("k_block must be >= 0")
+        if self.max_slices is not None and self.max_slices < 1:
+            raise ValueError("max_slices must be >= 1")
+        if self.accumulation_order not in _ACC_ORDERS:
+            raise ValueError(f"accumulation_order must be one of {_ACC_ORDERS}")
+        if self.pair_cutoff is not None and self.pair_cutoff < 0:
+            raise ValueError("pair_cutoff must be >= 0")
+
+
+@dataclass
+class BlockStats:
+    k_lo: int
+    k_hi: int
+    s_x: int
+    s_y: int
+    gemms: int
+
+
+@dataclass
+class OzStats:
+    """Cost tallies with the reference's schema (ozgemm.py:84-112).  Wall times
+    are CUDA-event times; accumulation is fused into the GEMM epilogue, so
+    ``t_accum`` is 0 and ``t_gemm`` covers product + accumulation."""
+
+    blocks: list = field(default_factory=list)
+    gemm_count: int = 0
+    slicing_ops: int = 0
+    gemm_ops: int = 0
+    accum_ops: int = 0
+    t_slice: float = 0.0
+    t_gemm: float = 0.0
+    t_accum: float = 0.0
+
+    def as_dict(self):
+        return {
+            "blocks": [vars(b) for b in self.blocks],
+            "gemm_count": self.gemm_count,
+            "element_ops": {"slicing": self.slicing_ops, "gemm": self.gemm_ops,
+                            "accumulation": self.accum_ops},
+            "wall_s": {"slicing": self.t_slice, "gemm": self.t_gemm, "accumulation": self.t_accum},
+        }
+
+
+@dataclass
+class OzResult:
+    C: object
+    stats: OzStats
+
+
+def _blocks(k: int, k_block: int):
+    if k_block == 0:
+        return [(0, k)]
+    return [(lo, min(lo + k_block, k)) for lo in range(0, k, k_block)]
+
+
+def pair_order(sx: int, sy: int, order: str = "smallest-first", cutoff: int | None = None):
+    """The pair sequence the fused kernel walks (ozgemm.py:179-183), restricted
+    to p + q <= cutoff.  Host mirror of PairIter in oz_pair_gemm.cu."""
+    pairs = [(p, q) for p in range(sx) for q in range(sy) if cutoff is None or p + q <= cutoff]
+    if order == "smallest-first":
+        pairs.sort(key=lambda pq: (-(pq[0] + pq[1]), pq[0], pq[1]))
+    else:
+        pairs.sort(key=lambda pq: (pq[0] + pq[1], pq[0], pq[1]))
+    return pairs
+
+
+def _check_accumulator(params, kb: int):
+    # Slice coefficients sit on the 2^(rho-53) grid with |c| <= 1, so every
+    # partial sum of kb products is exact in the tensor cores' FP32 accumulator
+    # iff kb <= 2^(24 + 2(rho-53)).  Guaranteed for type3 with m3 <= 24 by the
+    # choice of gamma; wider accumulators (type3 = fp64) need chunked
+    # accumulation, which this build does not implement.
+    if kb > 2.0 ** (24 + 2 * (params.rho - 53)):
+        raise NotImplementedError(
+            f"k-block {kb} exceeds the exact range of the FP32 tensor-core accumulator "
+            f"for rho={params.rho}; use type3 with <= 24 significand bits or a smaller k_block")
+
+
+def _as_device(M, torch):
+    if isinstance(M, torch.Tensor):
+        return M.to(device="cuda", dtype=torch.float64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(M, dtype=np.float64))).to("cuda")
+
+
+def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True):
+    """C = A @ B for CUDA float64 tensors; returns (C, OzStats).  No host copies
+    of operands or result (the timed hot path of bench.py)."""
+    torch = _lib.require_cuda()
+    if A.ndim != 2 or B.ndim != 2 or A.shape[1] != B.shape[0]:
+        raise DimensionError(f"cannot multiply shapes {tuple(A.shape)} and {tuple(B.shape)}")
+    m, k = A.shape
+    n = B.shape[1]
+    if cfg.k_block > k:
+        raise ValueError("k_block exceeds k")
+    emu = bool(cfg.fp64_emulation)
+    order = 0 if cfg.accumulation_order == "smallest-first" else 1
+    cutoff = -1 if cfg.pair_cutoff is None else int(cfg.pair_cutoff)
+    stats = OzStats()
+    C = out if out is not None else torch.empty((m, n), dtype=torch.float64, device=A.device)
+    sp = _lib.stream_ptr(torch)
+    flags = torch.zeros(1, dtype=torch.int32, device=A.device)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timing else None
+    t_slice = t_gemm = 0.0
+    for bi, (lo, hi) in enumerate(_blocks(k, cfg.k_block)):
+        kb = hi - lo
+        params = compute_params(53, cfg.type2.mant_bits, cfg.type3.mant_bits, kb)
+        if not params.feasible:
+            raise SlicingInfeasible(
+                f"slice width {params.slice_width} < 0 for m2={params.m2}, m3={params.m3}, k={kb}")
+        _check_accumulator(params, kb)
+        if timing:
+            ev[0].record()
+        sa, _ = split_rows_device(A[:, lo:hi], cfg.type2, params, emu)
+        sb, _ = split_rows_device(transpose_device(B[lo:hi, :]), cfg.type2, params, emu)
+        if timing:
+            ev[1].record()
+        sx = min(sa.s, cfg.max_slices or sa.s)
+        sy = min(sb.s, cfg.max_slices or sb.s)
+        kept = len(pair_order(sx, sy, cfg.accumulation_order, cfg.pair_cutoff)) \
+            if cfg.pair_cutoff is not None else sx * sy
+        stats.slicing_ops += 4 * (sa.s * m * kb + sb.s * kb * n)
+        stats.blocks.append(BlockStats(lo, hi, sx, sy, kept))
+        stats.gemm_count += kept
+        stats.gemm_ops += 2 * m * n * kb * kept
+        stats.accum_ops += 2 * m * n * kept + m * n
+        tca = tcb = None
+        if cfg.skip_zero_pairs and m and n:
+            tca = torch.empty((m + 127) // 128, dtype=torch.int32, device=A.device)
+            tcb = torch.empty((n + 127) // 128, dtype=torch.int32, device=A.device)
+            _lib.call("oz_tile_counts", sa.row_cnt.data_ptr(), m, tca.data_ptr(), sp)
+            _lib.call("oz_tile_counts", sb.row_cnt.data_ptr(), n, tcb.data_ptr(), sp)
+        _lib.call("oz_pair_gemm",
+                  sa.planes.data_ptr() if sa.s else None, sb.planes.data_ptr() if sb.s else None,
+                  sa.ld, sb.ld, sa.s, sb.s,
+                  sa.expo.data_ptr() if sa.s else None, sb.expo.data_ptr() if sb.s else None,
+                  tca.data_ptr() if tca is not None else None,
+                  tcb.data_ptr() if tcb is not None else None,
+                  m, n, kb, sx, sy, _lib.FMT_CODE[cfg.type2.name], order, cutoff, int(emu),
+                  int(bi > 0), C.data_ptr(), n, flags.data_ptr(), sp)
+        if timing:
+            ev[2].record()
+            ev[2].synchronize()
+            t_slice += ev[0].elapsed_time(ev[1]) / 1e3
+            t_gemm += ev[1].elapsed_time(ev[2]) / 1e3
+    f = int(flags.item()) & 0xFFFFFFFF
+    _lib.raise_for_flags(f, "pair gemm")
+    stats.t_slice, stats.t_gemm = t_slice, t_gemm
+    return C, stats
+
+
+def oz_gemm(A, B, cfg: GemmConfig) -> OzResult:
+    """C = A @ B with FP64 accuracy using only tensor-core slice GEMMs.
+
+    Same contract as ``ozdgemm.oz_gemm`` (ozgemm.py:143-211).  numpy inputs are
+    copied to the GPU and C comes back as a numpy array; CUDA tensors stay on
+    the device and C is a CUDA tensor."""
+    torch = _lib.require_cuda()
+    is_torch = isinstance(A, torch.Tensor) and isinstance(B, torch.Tensor)
+    if not is_torch:
+        A = np.asarray(A, dtype=np.float64)
+        B = np.asarray(B, dtype=np.float64)
+    if A.ndim != 2 or B.ndim != 2 or A.shape[1] != B.shape[0]:
+        raise DimensionError(f"cannot multiply shapes {tuple(A.shape)} and {tuple(B.shape)}")
+    Ad, Bd = _as_device(A, torch), _as_device(B, torch)
+    C, stats = oz_gemm_device(Ad, Bd, cfg)
+    return OzResult(C if is_torch else C.cpu().numpy(), stats)
+
+
+def oz_gemm_count(m: int, n: int, k: int, cfg: GemmConfig) -> int:
+    """Predicted GEMMs for fully filled mantissas (ozgemm.py:214-224)."""
+    kb = cfg.k_block if cfg.k_block else k
+    per_block = predict_gemm_count(53, cfg.type2.mant_bits, cfg.type3.mant_bits, kb)
+    if per_block is None:
+        raise SlicingInfeasible(f"{cfg.type2.name}/{cfg.type3.name} infeasible at k_block={kb}")
+    return -(-k // kb) * per_block
+
+
+def transpose(M):
+    """Exact element permutation (ozgemm.py:121-123); on the GPU for CUDA tensors."""
+    try:
+        import torch
+
+        if isinstance(M, torch.Tensor) and M.is_cuda:
+            return transpose_device(M.to(torch.float64))
+    except ImportError:
+        pass
+    return np.ascontiguousarray(np.asarray(M).T)

@@ -1,0 +1,230 @@
+"""Error-free slicing of FP64 matrices along the inner dimension — B200 backend.
+
+Host-side planning mirrors ``ozdgemm.slicing`` (slicing.py:45-97): the same
+``SlicingParams`` / ``compute_params`` / ``predict_*`` contract.  The slicing
+itself (slicing.py:128-206) runs on the GPU in ``oz_split.cu``:
+
+  1. count pass  (``oz_split_count``): per-row slice counts, the global slice
+     count s, validation flags;
+  2. write pass  (``oz_split_rows``): exactly s planes of FP8/FP16 codes,
+     K-major ``[s][rows][ld]``, plus int32 exponents ``[s][rows]``.
+
+Columns of B are sliced by transposing B on the device first (the reference
+does the same transpose on the host, slicing.py:199-203).  ``slice_matrix``
+returns a reference-compatible ``SliceSet`` (float64 coefficient planes and
+integer exponents) decoded from the device planes; ``oz_gemm`` keeps the
+device planes (``DeviceSlices``) and never decodes them.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import SlicingInfeasible
+from .formats import FormatSpec, decode_codes
+
+__all__ = [
+    "SlicingInfeasible", "SlicingParams", "SliceSet", "DeviceSlices", "compute_params",
+    "predict_slice_count", "predict_gemm_count", "slice_vector", "slice_matrix", "split_rows_device",
+]
+
+
+@dataclass(frozen=True)
+class SlicingParams:
+    """Slicing constants for significand widths m1 (input), m2 (slice storage),
+    m3 (accumulator) at inner dimension k (slicing.py:45-69)."""
+
+    m1: int
+    m2: int
+    m3: int
+    k: int
+    gamma: int
+    xi: int
+    rho: int
+    slice_width: int = field(init=False)
+
+    def __post_init__(self):
+        object.__setattr__(self, "slice_width", self.m1 - self.rho)
+
+    @property
+    def feasible(self) -> bool:
+        return self.slice_width >= 0
+
+
+def compute_params(m1: int, m2: int, m3: int, k: int) -> SlicingParams:
+    """gamma = ceil(m1 - (m3 - log2 k)/2), xi = m1 - m2, rho = max(gamma, xi)
+    (slicing.py:72-81; paper Eqs. for the error-free accumulation bound)."""
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    if min(m1, m2, m3) < 1:
+        raise ValueError("significand bit counts must be >= 1")
+    gamma = math.ceil(m1 - (m3 - math.log2(k)) / 2)
+    xi = m1 - m2
+    return SlicingParams(m1, m2, m3, k, gamma, xi, max(gamma, xi))
+
+
+def predict_slice_count(params: SlicingParams):
+    """Slices for a fully filled m1-bit significand (slicing.py:84-88), or None."""
+    if not params.feasible:
+        return None
+    return -(-params.m1 // (params.slice_width + 1))
+
+
+def predict_gemm_count(m1: int, m2: int, m3: int, k: int):
+    """Square of the predicted slice count (slicing.py:91-97), or None."""
+    s = predict_slice_count(compute_params(m1, m2, m3, k))
+    return None if s is None else s * s
+
+
+@dataclass
+class SliceSet:
+    """Reference-compatible slices (slicing.py:100-116): ``coeff[p]`` has the
+    input's shape with exact float64 coefficient values, ``expo[p]`` one int per
+    row ("rows") or column ("cols")."""
+
+    orientation: str
+    s: int
+    coeff: list
+    expo: list
+    params: SlicingParams
+    fmt: FormatSpec
+
+
+@dataclass
+class DeviceSlices:
+    """Slices resident in HBM, laid out for TMA: ``planes`` uint8
+    ``[s, rows, ld * elem_bytes]`` (K-major codes, zero padded), ``expo`` int32
+    ``[s, rows]``, ``row_cnt`` int32 ``[rows]`` (per-row slice counts)."""
+
+    planes: object
+    expo: object
+    row_cnt: object
+    s: int
+    rows: int
+    kb: int
+    ld: int
+    fmt: FormatSpec
+
+    def codes(self):
+        """Codes as a [s, rows, kb] uint8/uint16 torch tensor view."""
+        import torch
+
+        v = self.planes if _lib.ELEM_BYTES[self.fmt.name] == 1 else self.planes.view(torch.int16)
+        return v[:, :, : self.kb]
+
+
+def _fmt_code(fmt: FormatSpec) -> int:
+    if fmt.name not in _lib.FMT_CODE:
+        raise NotImplementedError(
+            f"slice format {fmt.name!r} has no tensor-core path on sm_100a in this build "
+            f"(supported: {', '.join(_lib.FMT_CODE)})")
+    return _lib.FMT_CODE[fmt.name]
+
+
+def split_rows_device(X, fmt: FormatSpec, params: SlicingParams, emu: bool, stream=None,
+                      check: bool = True) -> tuple[DeviceSlices, int]:
+    """Slice every row of the CUDA float64 matrix view X (rows x kb, unit
+    column stride) on the GPU.  Returns (slices, flags); raises the reference's
+    exceptions when ``check``."""
+    torch = _lib.require_cuda()
+    if not params.feasible:
+        raise SlicingInfeasible(
+            f"slice width {params.slice_width} < 0 for m2={params.m2}, m3={params.m3}, k={params.k}")
+    code = _fmt_code(fmt)
+    rows, kb = X.shape
+    if X.dtype != torch.float64 or X.stride(1) != 1:
+        raise ValueError("split_rows_device expects a float64 view with unit column stride")
+    ldx = X.stride(0) if rows > 1 else kb
+    dev = X.device
+    sp = stream if stream is not None else _lib.stream_ptr(torch)
+    eb = _lib.ELEM_BYTES[fmt.name]
+    ld = -(-kb // (16 // eb)) * (16 // eb)
+    row_cnt = torch.zeros(max(rows, 1), dtype=torch.int32, device=dev)
+    small = torch.zeros(2, dtype=torch.int32, device=dev)  # [s_max, flags]
+    _lib.call("oz_split_count", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu),
+              row_cnt.data_ptr(), small.data_ptr(), small.data_ptr() + 4, sp)
+    s_max, flags = (int(v) for v in small.cpu().tolist())
+    flags &= 0xFFFFFFFF
+    if check:
+        _lib.raise_for_flags(flags, "split")
+    planes = torch.empty((s_max, rows, ld * eb), dtype=torch.uint8, device=dev)
+    expo = torch.empty((s_max, rows), dtype=torch.int32, device=dev)
+    if s_max > 0 and rows > 0:
+        small.zero_()
+        _lib.call("oz_split_rows", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu), s_max,
+                  planes.data_ptr(), ld, expo.data_ptr(), row_cnt.data_ptr(), small.data_ptr() + 4, sp)
+    return DeviceSlices(planes, expo, row_cnt[:rows], s_max, rows, kb, ld, fmt), flags
+
+
+def _to_device_f64(M):
+    torch = _lib.require_cuda()
+    if isinstance(M, torch.Tensor):
+        t = M.to(device="cuda", dtype=torch.float64)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(M, dtype=np.float64))).to("cuda")
+    return t.contiguous()
+
+
+def transpose_device(X):
+    """Device transpose (kernel ``oz_transpose``) of a 2-D float64 CUDA tensor."""
+    torch = _lib.require_cuda()
+    rows, cols = X.shape
+    if X.stride(1) != 1:
+        X = X.contiguous()
+    out = torch.empty((cols, rows), dtype=torch.float64, device=X.device)
+    if rows and cols:
+        _lib.call("oz_transpose", X.data_ptr(), rows, cols, X.stride(0) if rows > 1 else cols,
+                  out.data_ptr(), rows, _lib.stream_ptr(torch))
+    return out
+
+
+def slice_matrix(M, orientation: str, fmt: FormatSpec, params: SlicingParams,
+                 arith: str = "fp64") -> SliceSet:
+    """GPU replacement of ``ozdgemm.slice_matrix`` (slicing.py:190-206).
+
+    "rows" slices each row (left operand); "cols" each column (right operand).
+    ``arith`` selects hardware FP64 ("fp64") or the integer-only emulation
+    ("emu") inside the split kernel; both give identical bits."""
+    torch = _lib.require_cuda()
+    is_torch = isinstance(M, torch.Tensor)
+    if not is_torch:
+        M = np.asarray(M, dtype=np.float64)
+    if M.ndim != 2:
+        raise ValueError("slice_matrix expects a 2-D matrix")
+    if orientation not in ("rows", "cols"):
+        raise ValueError("orientation must be 'rows' or 'cols'")
+    if arith not in ("fp64", "emu"):
+        raise ValueError("arith must be 'fp64' or 'emu'")
+    X = _to_device_f64(M)
+    if orientation == "cols":
+        X = transpose_device(X)
+    ds, _ = split_rows_device(X, fmt, params, arith == "emu")
+    return device_to_sliceset(ds, orientation, params, as_torch=is_torch)
+
+
+def device_to_sliceset(ds: DeviceSlices, orientation: str, params: SlicingParams,
+                       as_torch: bool = False) -> SliceSet:
+    """Decode device planes into the reference's SliceSet representation."""
+    torch = _lib.require_cuda()
+    codes = ds.codes().cpu().numpy()
+    vals = decode_codes(codes if codes.dtype == np.uint8 else codes.view(np.uint16), ds.fmt.name)
+    expo = ds.expo.cpu().numpy().astype(np.int64)
+    coeff = [vals[p] if orientation == "rows" else np.ascontiguousarray(vals[p].T) for p in range(ds.s)]
+    expos = [expo[p] for p in range(ds.s)]
+    if as_torch:
+        coeff = [torch.from_numpy(c).cuda() for c in coeff]
+        expos = [torch.from_numpy(e).cuda() for e in expos]
+    return SliceSet(orientation, ds.s, coeff, expos, params, ds.fmt)
+
+
+def slice_vector(x, fmt: FormatSpec, params: SlicingParams, arith: str = "fp64"):
+    """Slice one length-k vector (slicing.py:180-187)."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.ndim != 1:
+        raise ValueError("slice_vector expects a 1-D vector")
+    ss = slice_matrix(x[None, :], "rows", fmt, params, arith)
+    return [c[0] for c in ss.coeff], [int(e[0]) for e in ss.expo]

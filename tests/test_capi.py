@@ -1,0 +1,104 @@
+"""The C-ABI library (no GPU needed): it loads, exports every entry point that
+include/oz_b200.h declares, the ctypes signatures cover exactly those, and the
+emulated-FP64 kernels contain no FP64 arithmetic in their SASS."""
+
+import re
+import shutil
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "oz_b200.h"
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__
+
+    __graft_entry__.build()
+    from paper_2508_00441_b200 import _lib
+
+    return _lib.load()
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(oz_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_header_declares_expected_entry_points():
+    names = declared_functions()
+    for must in ("oz_split_count", "oz_split_rows", "oz_pair_gemm", "oz_lp_gemm", "oz_transpose"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+
+
+def test_ctypes_signatures_cover_header(lib):
+    from paper_2508_00441_b200 import _lib
+
+    assert sorted(_lib.SIGNATURES) == declared_functions()
+
+
+def test_version_and_strerror_without_gpu(lib):
+    assert b"sm_100a" in lib.oz_version()
+    assert lib.oz_strerror(0) == b"ok"
+    assert b"unsupported" in lib.oz_strerror(2)
+
+
+def test_argument_errors_return_status_without_gpu(lib):
+    # null / negative arguments are rejected before any CUDA call
+    assert lib.oz_transpose(None, -1, 2, 2, None, 2, None) == 1
+    assert lib.oz_split_count(None, 4, 8, 8, 9, 49, 0, None, None, None, None) == 2  # bad type2
+    assert lib.oz_pair_gemm(None, None, 16, 16, 1, 1, None, None, None, None, 4, 4, 16, 2, 1, 0, 0, -1, 0, 0,
+                            None, 4, None, None) == 1
+
+
+def _sass_of(lib_path, kernel_substr):
+    if not shutil.which("cuobjdump") and not Path("/usr/local/cuda/bin/cuobjdump").exists():
+        pytest.skip("cuobjdump not available")
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    out = subprocess.run([exe, "-sass", str(lib_path)], check=True, capture_output=True, text=True).stdout
+    funcs = {}
+    cur = None
+    for line in out.splitlines():
+        m = re.match(r"\s*Function : (\S+)", line)
+        if m:
+            cur = m.group(1)
+            funcs[cur] = []
+        elif cur:
+            funcs[cur].append(line)
+    sel = {k: v for k, v in funcs.items() if kernel_substr(k)}
+    assert sel, "kernel not found in SASS"
+    return sel
+
+
+FP64_OPS = re.compile(r"\b(DFMA|DADD|DMUL|DSETP|DMNMX|DSET|F2F\.F64|F2F\.F32\.F64|I2F\.F64|F2I\.F64|DRCP|DMMA)\b")
+
+
+def test_emulated_kernels_have_no_fp64_arithmetic(lib):
+    from paper_2508_00441_b200 import _lib
+
+    # pair_gemm_kernel<true> -> _ZN2oz16pair_gemm_kernelILb1EE... ; split_rows_kernel<E, W, true>
+    sel = _sass_of(_lib.LIB_PATH, lambda k: ("pair_gemm_kernelILb1E" in k) or
+                   (re.search(r"split_rows_kernelILi\d+ELb[01]ELb1E", k) is not None))
+    assert len(sel) >= 3
+    for name, lines in sel.items():
+        bad = [ln for ln in lines if FP64_OPS.search(ln)]
+        assert not bad, f"{name} contains FP64 arithmetic: {bad[:3]}"
+
+
+def test_hw_kernels_do_use_fp64_and_tensor_cores(lib):
+    from paper_2508_00441_b200 import _lib
+
+    sel = _sass_of(_lib.LIB_PATH, lambda k: "pair_gemm_kernelILb0E" in k)
+    body = "\n".join(next(iter(sel.values())))
+    assert "DADD" in body
+    assert re.search(r"UTC[QH]MMA", body), "tcgen05.mma missing"
+    assert "UTMALDG" in body, "TMA load missing"
+    assert "LDTM" in body, "tcgen05.ld missing"

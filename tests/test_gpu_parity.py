@@ -1,0 +1,116 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle,
+bit for bit — slices, exponents, per-row counts, s, and the final C."""
+
+import numpy as np
+import pytest
+
+from conftest import bits, spread_matrix
+
+pytestmark = pytest.mark.gpu
+
+
+def _oz():
+    import paper_2508_00441_b200 as oz
+
+    return oz
+
+
+@pytest.mark.parametrize("fmt", ["fp8e4m3", "fp16", "bf16", "fp8e5m2"])
+@pytest.mark.parametrize("emu", [False, True])
+@pytest.mark.parametrize("shape,phi", [((7, 33), 0.5), ((64, 1000), 4.0), ((130, 4096), 1.0)])
+def test_split_rows_bitwise(cuda, fmt, emu, shape, phi):
+    import oracle
+
+    oz = _oz()
+    rng = np.random.default_rng(hash((fmt, emu, shape)) % 2**32)
+    X = spread_matrix(rng, *shape, phi)
+    kb = shape[1]
+    params = oz.compute_params(53, oz.get_format(fmt).mant_bits, 24, kb)
+    ss = oz.slice_matrix(X, "rows", oz.get_format(fmt), params, "emu" if emu else "fp64")
+    coeff, expo, _, s, flags = oracle.split_rows(X, params.rho, emu)
+    assert flags == 0
+    assert ss.s == s
+    for p in range(s):
+        assert np.array_equal(bits(ss.coeff[p]), bits(coeff[p])), f"coeff plane {p}"
+        assert np.array_equal(ss.expo[p], expo[p].astype(np.int64)), f"expo plane {p}"
+
+
+def test_split_cols_bitwise(cuda):
+    import oracle
+
+    oz = _oz()
+    rng = np.random.default_rng(5)
+    M = spread_matrix(rng, 300, 77, 2.0)
+    params = oz.compute_params(53, 4, 24, 300)
+    ss = oz.slice_matrix(M, "cols", oz.get_format("fp8e4m3"), params)
+    coeff, expo, s, flags = oracle.slice_matrix(M, "cols", params.rho)
+    assert ss.s == s
+    for p in range(s):
+        assert np.array_equal(bits(ss.coeff[p]), bits(coeff[p]))
+        assert np.array_equal(ss.expo[p], expo[p])
+
+
+CASES = [
+    # m, n, k, phi, type2, type3, k_block, emu, max_slices, order, cutoff
+    (128, 128, 128, 0.5, "fp8e4m3", "fp32", 0, False, None, "smallest-first", None),
+    (192, 160, 320, 0.5, "fp8e4m3", "fp32", 0, False, None, "smallest-first", None),
+    (100, 77, 333, 4.0, "fp8e4m3", "fp32", 0, False, None, "smallest-first", None),
+    (256, 256, 1024, 0.5, "fp8e4m3", "fp32", 0, True, None, "smallest-first", None),
+    (200, 136, 640, 1.0, "fp8e4m3", "fp32", 256, False, None, "smallest-first", None),
+    (129, 257, 200, 2.0, "fp8e4m3", "fp32", 0, False, 5, "largest-first", None),
+    (256, 128, 512, 0.5, "fp16", "fp32", 0, False, None, "smallest-first", None),
+    (160, 96, 700, 4.0, "fp16", "fp32", 300, True, None, "smallest-first", None),
+    (128, 128, 256, 0.5, "fp8e4m3", "fp16", 0, False, None, "smallest-first", None),
+    (128, 200, 512, 0.5, "fp8e4m3", "fp32", 0, False, None, "smallest-first", 12),
+    (64, 64, 96, 1.0, "bf16", "fp32", 0, False, None, "smallest-first", None),
+    (64, 64, 96, 1.0, "fp8e5m2", "fp32", 0, False, None, "largest-first", None),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}x{c[1]}x{c[2]}-{c[4]}-{c[5]}-kb{c[6]}-emu{int(c[7])}"
+                                             f"-ms{c[8]}-{c[9][:5]}-cut{c[10]}" for c in CASES])
+@pytest.mark.parametrize("skip", [True, False])
+def test_oz_gemm_bitwise(cuda, case, skip):
+    import oracle
+
+    oz = _oz()
+    m, n, k, phi, t2, t3, kbk, emu, ms, order, cut = case
+    rng = np.random.default_rng(m * 7 + n * 13 + k)
+    A = spread_matrix(rng, m, k, phi)
+    B = spread_matrix(rng, k, n, phi)
+    cfg = oz.GemmConfig(oz.get_format(t2), oz.get_format(t3), k_block=kbk, fp64_emulation=emu,
+                        max_slices=ms, accumulation_order=order, pair_cutoff=cut, skip_zero_pairs=skip)
+    res = oz.oz_gemm(A, B, cfg)
+    Cref, info = oracle.oz_gemm(A, B, t2, t3, kbk, emu, ms, order, cut)
+    assert info["flags"] == 0
+    assert [(b.k_lo, b.k_hi, b.s_x, b.s_y) for b in res.stats.blocks] == info["blocks"]
+    nbad = int(np.sum(bits(res.C) != bits(Cref)))
+    assert nbad == 0, f"{nbad}/{m * n} entries differ"
+
+
+def test_device_tensors_roundtrip(cuda):
+    torch = cuda
+    oz = _oz()
+    rng = np.random.default_rng(3)
+    A = spread_matrix(rng, 256, 512, 0.5)
+    B = spread_matrix(rng, 512, 128, 0.5)
+    cfg = oz.GemmConfig(oz.get_format("fp8e4m3"), oz.get_format("fp32"))
+    r1 = oz.oz_gemm(A, B, cfg)
+    r2 = oz.oz_gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), cfg)
+    assert isinstance(r2.C, torch.Tensor) and r2.C.is_cuda
+    assert np.array_equal(bits(r1.C), bits(r2.C.cpu().numpy()))
+
+
+def test_lp_gemm_exact_on_slices(cuda):
+    oz = _oz()
+    rng = np.random.default_rng(11)
+    A = spread_matrix(rng, 130, 256, 0.5)
+    B = spread_matrix(rng, 256, 70, 0.5)
+    f = oz.get_format("fp8e4m3")
+    params = oz.compute_params(53, 4, 24, 256)
+    sa = oz.slice_matrix(A, "rows", f, params)
+    sb = oz.slice_matrix(B, "cols", f, params)
+    for p in (0, sa.s - 1):
+        for q in (0, sb.s - 1):
+            G = oz.lp_gemm(oz.LpMatrix(sa.coeff[p], f), oz.LpMatrix(sb.coeff[q], f), oz.get_format("fp32"))
+            assert np.array_equal(G, sa.coeff[p] @ sb.coeff[q])
