@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--emu", action="store_true")
     ap.add_argument("--max-slices", type=int, default=None)
     ap.add_argument("--pair-cutoff", type=int, default=None)
-    ap.add_argument("--no-skip", action="store_true", help="disable (result-neutral) zero-pair skipping")
+    ap.add_argument("--skip-zero-pairs", action="store_true", help="enable (result-neutral) zero-pair skipping")
     ap.add_argument("--no-extras", action="store_true", help="skip accuracy / cuBLAS / CPU-baseline legs")
     ap.add_argument("--cpu-rows", type=int, default=64, help="CPU-baseline sample: rows of C")
     ap.add_argument("--cpu-cols", type=int, default=512, help="CPU-baseline sample: cols of C")
@@ -206,6 +206,15 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def oz_pace_slack():
+    try:
+        from paper_2508_00441_b200.ozgemm import PACE_SLACK
+
+        return PACE_SLACK
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def workload_config(args, per_gpu=False):
     opts = []
     if args.emu:
@@ -220,7 +229,7 @@ def workload_config(args, per_gpu=False):
                         + (", ".join(opts) if opts else "reference defaults (all pairs, smallest-first, HW FP64)"),
             "m": args.n, "n": args.n, "k": args.n, "phi": args.phi, "type2": args.type2, "type3": args.type3,
             "k_block": args.kblock, "fp64_emulation": args.emu, "max_slices": args.max_slices,
-            "pair_cutoff": args.pair_cutoff, "skip_zero_pairs": not args.no_skip,
+            "pair_cutoff": args.pair_cutoff, "skip_zero_pairs": args.skip_zero_pairs, "pace_slack": oz_pace_slack(),
             "l2": "inputs (2 x 512 MiB at n=8192) exceed the 126 MB L2; no flush",
             "parallelism": "2-D C tiles" if args.gpus > 1 else "1 GPU"}
 
@@ -246,7 +255,7 @@ def main():
     n = args.n
     cfg = oz.GemmConfig(oz.get_format(args.type2), oz.get_format(args.type3), k_block=args.kblock,
                         fp64_emulation=args.emu, max_slices=args.max_slices, pair_cutoff=args.pair_cutoff,
-                        skip_zero_pairs=not args.no_skip)
+                        skip_zero_pairs=args.skip_zero_pairs)
 
     # ---- inputs: this rank's C tile is n x n; A row-panel n x n, B column-panel n x n ----
     from paper_2508_00441_b200.distributed import TileGrid

@@ -84,12 +84,17 @@ int oz_tile_counts(const int32_t* row_cnt, int64_t rows, int32_t* tile_cnt, void
  *   pair skipping).  order: 0 smallest-first, 1 largest-first.  pair_cutoff < 0
  *   keeps all pairs (reference semantics); >= 0 keeps p+q <= pair_cutoff
  *   (opt-in extension).  emu: integer-only FP64 epilogue.  accumulate: 0 writes
- *   C = Cb, 1 writes C = C + Cb. */
+ *   C = Cb, 1 writes C = C + Cb.
+ *   pace_ws / pace_ws_bytes / pace_slack: optional device scratch (4 bytes per
+ *   tile-wave per pair) enabling cross-CTA pacing — resident CTAs stay within
+ *   pace_slack pair-steps of each other so slice panels are reused from L2
+ *   (scheduling only; results are identical).  Ignored when tile_cnt_a != NULL
+ *   or pace_slack <= 0. */
 int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64_t ld_b, int planes_a,
                  int planes_b, const int32_t* expo_a, const int32_t* expo_b, const int32_t* tile_cnt_a,
                  const int32_t* tile_cnt_b, int64_t m, int64_t n, int64_t kb, int sx, int sy, int type2,
                  int order, int pair_cutoff, int emu, int accumulate, double* C, int64_t ldc, uint32_t* flags,
-                 void* stream);
+                 void* pace_ws, int64_t pace_ws_bytes, int pace_slack, void* stream);
 
 /* One slice-pair product D (m x n, fp32) = A (m x k) . B (n x k)^T on tcgen05 —
  * replaces lpgemm.lp_gemm (lpgemm.py:93-120) for slice operands (exact). */

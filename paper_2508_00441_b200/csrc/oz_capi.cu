@@ -170,7 +170,7 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
                  int planes_b, const int32_t* expo_a, const int32_t* expo_b, const int32_t* tile_cnt_a,
                  const int32_t* tile_cnt_b, int64_t m, int64_t n, int64_t kb, int sx, int sy, int type2,
                  int order, int pair_cutoff, int emu, int accumulate, double* C, int64_t ldc, uint32_t* flags,
-                 void* stream) {
+                 void* pace_ws, int64_t pace_ws_bytes, int pace_slack, void* stream) {
   LpFormat f;
   uint32_t idf;
   if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
@@ -204,6 +204,24 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   const size_t smem = oz::pair_gemm_smem_bytes();
   const int tiles = P.tiles_m * P.tiles_n;
   const int grid = tiles < num_sms() ? tiles : num_sms();
+  // Pacing needs an identical pair sequence in every tile (no skipping) and
+  // scratch counters; the caller passes them through oz_set_pacing().
+  P.step_ctr = nullptr; P.pace_slack = 0; P.pairs_per_tile = 0;
+  if (!tile_cnt_a && pace_ws && pace_slack > 0) {
+    int pairs = 0;
+    const int dmax = sx + sy - 2;
+    for (int p = 0; p < sx; ++p)
+      for (int q = 0; q < sy; ++q)
+        if (pair_cutoff < 0 || p + q <= (pair_cutoff < dmax ? pair_cutoff : dmax)) ++pairs;
+    const int waves = (tiles + grid - 1) / grid;
+    const size_t need = sizeof(uint32_t) * (size_t)waves * (size_t)pairs;
+    if (pairs > 0 && need <= pace_ws_bytes) {
+      cudaMemsetAsync(pace_ws, 0, need, st);
+      P.step_ctr = static_cast<uint32_t*>(pace_ws);
+      P.pace_slack = pace_slack;
+      P.pairs_per_tile = pairs;
+    }
+  }
   if (emu) {
     cudaFuncSetAttribute(oz::pair_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     oz::pair_gemm_kernel<true><<<grid, oz::kPThreads, smem, st>>>(ma, mb, P);

@@ -58,7 +58,23 @@ struct PairParams {
   int elem_bytes;            // 1: kind::f8f6f4, 2: kind::f16
   uint32_t fmt;              // idesc a/b format code
   uint32_t* flags;
+  // Cross-CTA pacing (L2 locality): producers of all resident CTAs stay within
+  // `pace_slack` pair-steps of each other.  step_ctr has waves*pairs_per_tile
+  // zeroed counters; nullptr disables pacing (required when tiles skip pairs).
+  uint32_t* step_ctr;
+  int pace_slack;
+  int pairs_per_tile;
 };
+
+OZ_DEVICE uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+OZ_DEVICE void red_release_gpu_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // Pair enumeration in reference order restricted to p < lp, q < lq, p+q <= cut.
 struct PairIter {
@@ -177,9 +193,20 @@ __global__ void __launch_bounds__(kPThreads, 1)
         int tm, tn, lp, lq;
         tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
         tile_limits(P, tm, tn, lp, lq);
+        const int wave = tile / gridDim.x;
         PairIter pi;
-        for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next()) {
+        int t = 0;
+        for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++t) {
           const int p = pi.p, q = pi.q();
+          if (P.step_ctr) {
+            // Wait until every CTA of the wave `pace_slack` steps back has issued its loads.
+            const int g = wave * P.pairs_per_tile + t - P.pace_slack;
+            if (g >= 0) {
+              const int gw = g / P.pairs_per_tile;
+              const uint32_t need = (uint32_t)min((int)gridDim.x, num_tiles - gw * (int)gridDim.x);
+              while (ld_acquire_gpu(P.step_ctr + g) < need) __nanosleep(32);
+            }
+          }
           for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
             const uint32_t st = it % kPStages;
             if (it >= (uint32_t)kPStages) mbar_wait(&s.empty[st], ((it / kPStages) - 1) & 1);
@@ -187,6 +214,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             tma_load_3d(s.a[st], &map_a, &s.full[st], kbi * kb_elems, tm * kPM, p, kEvictNormal);
             tma_load_3d(s.b[st], &map_b, &s.full[st], kbi * kb_elems, tn * kPN, q, kEvictNormal);
           }
+          if (P.step_ctr) red_release_gpu_add(P.step_ctr + wave * P.pairs_per_tile + t, 1u);
         }
       }
     }

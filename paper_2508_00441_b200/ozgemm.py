@@ -13,13 +13,16 @@ order, bitwise the same C.  Per inner-product block [lo, hi)
 Two opt-in extensions beyond the reference, both off by default:
   * ``pair_cutoff = d`` keeps only pairs with p + q <= d (a prefix-free subset
     of the reference order; ``d >= sx + sy - 2`` is exactly the reference);
-  * ``skip_zero_pairs`` (default on) skips pairs whose A- or B-slice is all zero
-    over a 128x128 output tile: such a term is +0 and Cb is never -0, so C is
-    bitwise unchanged (this is not an approximation).
+  * ``skip_zero_pairs`` skips pairs whose A- or B-slice is all zero over a
+    128x128 output tile: such a term is +0 and Cb is never -0, so C is bitwise
+    unchanged (this is not an approximation).  Off by default: tiles then walk
+    different pair sequences, which breaks the cross-CTA pacing that keeps the
+    slice panels L2-resident (measured slower at n = 8192, profiles/).
 """
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -36,6 +39,9 @@ __all__ = [
 
 _ACC_ORDERS = ("smallest-first", "largest-first")
 
+# Cross-CTA pacing slack in pair-steps (scheduling only; 0 disables).
+PACE_SLACK = int(os.environ.get("OZ_PACE_SLACK", "2"))
+
 
 @dataclass(frozen=True)
 class GemmConfig:
@@ -50,7 +56,7 @@ class GemmConfig:
     seed: int = 0
     # ---- extensions (defaults reproduce the reference bit for bit) ----
     pair_cutoff: int | None = None
-    skip_zero_pairs: bool = True
+    skip_zero_pairs: bool = False
 
     def __post_init__(self):
         if self.k_block < 0:
@@ -132,6 +138,16 @@ def _check_accumulator(params, kb: int):
             f"for rho={params.rho}; use type3 with <= 24 significand bits or a smaller k_block")
 
 
+_SMS = {}
+
+
+def _num_sms(torch) -> int:
+    d = torch.cuda.current_device()
+    if d not in _SMS:
+        _SMS[d] = torch.cuda.get_device_properties(d).multi_processor_count
+    return _SMS[d]
+
+
 def _as_device(M, torch):
     if isinstance(M, torch.Tensor):
         return M.to(device="cuda", dtype=torch.float64).contiguous()
@@ -185,6 +201,10 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True):
             tcb = torch.empty((n + 127) // 128, dtype=torch.int32, device=A.device)
             _lib.call("oz_tile_counts", sa.row_cnt.data_ptr(), m, tca.data_ptr(), sp)
             _lib.call("oz_tile_counts", sb.row_cnt.data_ptr(), n, tcb.data_ptr(), sp)
+        pace = None
+        if tca is None and PACE_SLACK > 0 and m and n:
+            waves = -(-(((m + 127) // 128) * ((n + 127) // 128)) // _num_sms(torch))
+            pace = torch.empty(waves * max(kept, 1), dtype=torch.int32, device=A.device)
         _lib.call("oz_pair_gemm",
                   sa.planes.data_ptr() if sa.s else None, sb.planes.data_ptr() if sb.s else None,
                   sa.ld, sb.ld, sa.s, sb.s,
@@ -192,7 +212,9 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True):
                   tca.data_ptr() if tca is not None else None,
                   tcb.data_ptr() if tcb is not None else None,
                   m, n, kb, sx, sy, _lib.FMT_CODE[cfg.type2.name], order, cutoff, int(emu),
-                  int(bi > 0), C.data_ptr(), n, flags.data_ptr(), sp)
+                  int(bi > 0), C.data_ptr(), n, flags.data_ptr(),
+                  pace.data_ptr() if pace is not None else None, pace.numel() * 4 if pace is not None else 0,
+                  PACE_SLACK, sp)
         if timing:
             ev[2].record()
             ev[2].synchronize()
