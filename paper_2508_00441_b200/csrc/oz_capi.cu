@@ -7,6 +7,7 @@
 #include "oz_dd_gemm.cu"
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -43,15 +44,15 @@ EncodeFn get_encode() {
   return fn;
 }
 
-// 3-D map over slice planes [planes][rows][ld] with a 128-byte x 128-row box, SWIZZLE_128B.
+// 3-D map over slice planes [planes][rows][ld] with a 128-byte x box_rows box, SWIZZLE_128B.
 int make_plane_map(CUtensorMap* map, const void* base, int elem_bytes, int64_t k, int64_t rows, int64_t planes,
-                   int64_t ld) {
+                   int64_t ld, int box_rows = 128) {
   EncodeFn enc = get_encode();
   if (!enc) return OZ_ETMAP;
   if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * elem_bytes) & 15)) return OZ_EINVAL;
   const cuuint64_t dims[3] = {(cuuint64_t)k, (cuuint64_t)rows, (cuuint64_t)planes};
   const cuuint64_t strides[2] = {(cuuint64_t)(ld * elem_bytes), (cuuint64_t)(ld * elem_bytes * rows)};
-  const cuuint32_t box[3] = {(cuuint32_t)(128 / elem_bytes), 128u, 1u};
+  const cuuint32_t box[3] = {(cuuint32_t)(128 / elem_bytes), (cuuint32_t)box_rows, 1u};
   const cuuint32_t estr[3] = {1u, 1u, 1u};
   const CUresult r =
       enc(map, elem_bytes == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3,
@@ -100,6 +101,31 @@ int launch_split(const oz::SplitParams& P, int emu, cudaStream_t st) {
     OZ_SPLIT_CASE(64)
   }
 #undef OZ_SPLIT_CASE
+  return launch_status();
+}
+
+template <bool kEmu, int kCta>
+int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const oz::PairParams& P, int units, cudaStream_t st) {
+  const size_t smem = oz::pair_gemm_smem_bytes<kCta>();
+  auto kern = oz::pair_gemm_kernel<kEmu, kCta>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(units * kCta));
+  cfg.blockDim = dim3(oz::kPThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCta;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, P);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "oz_b200: pair_gemm launch failed: %s\n", cudaGetErrorString(e));
+    return OZ_ECUDA;
+  }
   return launch_status();
 }
 
@@ -190,46 +216,48 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
     return launch_status();
   }
   if (!a_planes || !b_planes || !expo_a || !expo_b) return OZ_EINVAL;
-  CUtensorMap ma, mb;
-  int rc = make_plane_map(&ma, a_planes, f.bytes, kb, m, planes_a, ld_a);
-  if (rc) return rc;
-  rc = make_plane_map(&mb, b_planes, f.bytes, kb, n, planes_b, ld_b);
-  if (rc) return rc;
   oz::PairParams P{};
   P.expo_a = expo_a; P.expo_b = expo_b; P.tile_cnt_a = tile_cnt_a; P.tile_cnt_b = tile_cnt_b;
   P.C = C; P.ldc = ldc; P.m = (int)m; P.n = (int)n; P.kb = (int)kb; P.sx = sx; P.sy = sy;
   P.order = order; P.cutoff = pair_cutoff; P.accumulate = accumulate;
-  P.tiles_m = (int)((m + oz::kPM - 1) / oz::kPM); P.tiles_n = (int)((n + oz::kPN - 1) / oz::kPN);
   P.elem_bytes = f.bytes; P.fmt = idf; P.flags = flags;
-  const size_t smem = oz::pair_gemm_smem_bytes();
+  // CTA-pair (cta_group::2, 256x128 tiles) unless the problem has a single
+  // 128-row slab; OZ_CTA_GROUP=1|2 overrides (experiments).
+  int cta = m > oz::kPM ? 2 : 1;
+  if (const char* e = getenv("OZ_CTA_GROUP")) cta = atoi(e) == 1 ? 1 : 2;
+  CUtensorMap ma, mb;
+  int rc = make_plane_map(&ma, a_planes, f.bytes, kb, m, planes_a, ld_a, oz::kPM);
+  if (rc) return rc;
+  rc = make_plane_map(&mb, b_planes, f.bytes, kb, n, planes_b, ld_b, oz::kPN / cta);
+  if (rc) return rc;
+  P.tiles_m = (int)((m + oz::kPM * cta - 1) / (oz::kPM * cta));
+  P.tiles_n = (int)((n + oz::kPN - 1) / oz::kPN);
   const int tiles = P.tiles_m * P.tiles_n;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
+  const int units_max = num_sms() / cta;
+  const int units = tiles < units_max ? tiles : units_max;
   // Pacing needs an identical pair sequence in every tile (no skipping) and
-  // scratch counters; the caller passes them through oz_set_pacing().
+  // scratch counters (one per tile-wave and pair).
   P.step_ctr = nullptr; P.pace_slack = 0; P.pairs_per_tile = 0;
   if (!tile_cnt_a && pace_ws && pace_slack > 0) {
     int pairs = 0;
-    const int dmax = sx + sy - 2;
     for (int p = 0; p < sx; ++p)
       for (int q = 0; q < sy; ++q)
-        if (pair_cutoff < 0 || p + q <= (pair_cutoff < dmax ? pair_cutoff : dmax)) ++pairs;
-    const int waves = (tiles + grid - 1) / grid;
+        if (pair_cutoff < 0 || p + q <= pair_cutoff) ++pairs;
+    const int waves = (tiles + units - 1) / units;
     const size_t need = sizeof(uint32_t) * (size_t)waves * (size_t)pairs;
-    if (pairs > 0 && need <= pace_ws_bytes) {
+    if (pairs > 0 && need <= (size_t)pace_ws_bytes) {
       cudaMemsetAsync(pace_ws, 0, need, st);
       P.step_ctr = static_cast<uint32_t*>(pace_ws);
       P.pace_slack = pace_slack;
       P.pairs_per_tile = pairs;
     }
   }
-  if (emu) {
-    cudaFuncSetAttribute(oz::pair_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    oz::pair_gemm_kernel<true><<<grid, oz::kPThreads, smem, st>>>(ma, mb, P);
-  } else {
-    cudaFuncSetAttribute(oz::pair_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    oz::pair_gemm_kernel<false><<<grid, oz::kPThreads, smem, st>>>(ma, mb, P);
+  if (cta == 1) {
+    if (emu) return launch_pair<true, 1>(ma, mb, P, units, st);
+    return launch_pair<false, 1>(ma, mb, P, units, st);
   }
-  return launch_status();
+  if (emu) return launch_pair<true, 2>(ma, mb, P, units, st);
+  return launch_pair<false, 2>(ma, mb, P, units, st);
 }
 
 int oz_dd_gemm(const double* A, const double* B, double* C, int64_t m, int64_t n, int64_t k, void* stream) {

@@ -6,38 +6,50 @@
 //   ozgemm.py:192-193   T = ldexp(G, cA_p[i] + cB_q[j])     (_scale_terms_exact :132-140)
 //   ozgemm.py:194-197   Cb = Cb + T   (hardware FP64 or fp64emu.add_arrays)
 //   ozgemm.py:204-207   C  = C + Cb   (ascending blocks)
-// G never touches HBM.  Per 128 x 128 output tile (one CTA, persistent):
-//   warp 0      TMA producer: A_p / B_q k-blocks (128 B rows, SWIZZLE_128B) into a
-//               kStages-deep smem ring;
-//   warp 1      tcgen05.mma issuer (kind::f8f6f4 E4M3/E5M2 or kind::f16 F16/BF16,
-//               FP32 accumulate) into one of kAccBufs TMEM accumulators per pair;
-//               owns the TMEM allocation;
-//   warps 4..11 epilogue (setmaxnreg 232; warps 2-3 idle at 40 regs): tcgen05.ld the FP32 G, rebuild T = G * 2^(eA+eB) as an
+// G never touches HBM.  Persistent, warp-specialised; each CTA owns 128 output
+// rows x 128 columns of C per tile, with its FP64 Cb in the registers of 8
+// epilogue warps.  Two variants:
+//   kCta = 1: one CTA per 128x128 tile, tcgen05.mma.cta_group::1 (M=128, N=128);
+//   kCta = 2: a CTA pair (cluster of 2) per 256x128 tile, tcgen05.mma.cta_group::2
+//             (M=256, N=128) issued by the leader; each CTA stages its 128 A rows
+//             and HALF the B tile, so per-SM operand ingest drops from 256 to
+//             192 rows per k-block and twice the pipeline stages fit in smem.
+// Roles (384 threads, 3 warpgroups; setmaxnreg moves registers to the epilogue):
+//   warp 0      TMA producer: A_p / B_q k-blocks (128 B rows, SWIZZLE_128B);
+//   warp 1      TMEM owner + tcgen05.mma issuer (kind::f8f6f4 or kind::f16, FP32
+//               accumulate) into one of 4 TMEM accumulators per pair;
+//   warps 4-11  epilogue: tcgen05.ld the FP32 G, rebuild T = G * 2^(eA+eB) as an
 //               FP64 bit pattern with integer ops (exact), and add it into the
-//               register-resident FP64 Cb in the reference pair order, with
-//               __dadd_rn (HW mode) or the integer-only emu_add (EMU mode — this
-//               instantiation contains no DADD/DMUL/DFMA, see tests/test_sass.py).
-// Pairs whose A- or B-slice is all-zero over the tile (per-tile slice counts)
-// may be skipped: the term is +0 and Cb is never -0, so the result is unchanged.
+//               register-resident Cb in the reference pair order, with __dadd_rn
+//               (HW mode) or the integer-only emu_add (EMU mode — no DADD/DMUL/DFMA
+//               in that instantiation, tests/test_capi.py checks the SASS).
+// Producers of all resident CTAs are paced to within `pace_slack` pair-steps of
+// each other so concurrently used slice panels stay L2-resident.
 #include <type_traits>
 
 #include "oz_common.cuh"
 
 namespace oz {
 
-constexpr int kPM = 128, kPN = 128;        // output tile
-constexpr int kPStages = 5;                // smem ring depth
-constexpr int kPStageBytes = 2 * 128 * 128;
+constexpr int kPM = 128, kPN = 128;        // per-CTA output tile
 constexpr int kAccBufs = 4;                // TMEM accumulators (4 x 128 cols = 512)
 constexpr int kEpiWarps = 8;
-constexpr int kPThreads = 128 + 32 * kEpiWarps;  // WG0: TMA, MMA, 2 idle; WG1-2: epilogue
-constexpr int kMaxSy = 64;                 // B-exponent staging cap (planes)
+constexpr int kPThreads = 128 + 32 * kEpiWarps;
+constexpr int kMaxSy = 48;                 // B-exponent staging cap (planes)
 
+template <int kCta>
+struct PairCfg {
+  static constexpr int kBRows = kPN / kCta;                   // B rows staged per CTA
+  static constexpr int kStageBytes = (kPM + kBRows) * 128;    // per CTA
+  static constexpr int kStages = kCta == 1 ? 5 : 8;
+};
+
+template <int kCta>
 struct PairSmem {
-  alignas(1024) uint8_t a[kPStages][128 * 128];
-  alignas(1024) uint8_t b[kPStages][128 * 128];
+  alignas(1024) uint8_t a[PairCfg<kCta>::kStages][kPM * 128];
+  alignas(1024) uint8_t b[PairCfg<kCta>::kStages][PairCfg<kCta>::kBRows * 128];
   int32_t eb[kMaxSy][kPN];
-  uint64_t full[kPStages], empty[kPStages];
+  uint64_t full[PairCfg<kCta>::kStages], empty[PairCfg<kCta>::kStages];
   uint64_t acc_full[kAccBufs], acc_empty[kAccBufs];
   uint32_t tmem_base;
 };
@@ -45,8 +57,8 @@ struct PairSmem {
 struct PairParams {
   const int32_t* expo_a;     // [sx_planes][m]
   const int32_t* expo_b;     // [sy_planes][n]
-  const int32_t* tile_cnt_a; // [tiles_m] max slice count over the tile's rows (nullable = no skip)
-  const int32_t* tile_cnt_b; // [tiles_n]
+  const int32_t* tile_cnt_a; // [m/128] max slice count over the tile's rows (nullable = no skip)
+  const int32_t* tile_cnt_b; // [n/128]
   double* C;
   int64_t ldc;
   int m, n, kb;
@@ -54,7 +66,7 @@ struct PairParams {
   int order;                 // 0 = smallest-first, 1 = largest-first
   int cutoff;                // keep pairs with p+q <= cutoff  (< 0: keep all)
   int accumulate;            // 0: C = Cb (first block), 1: C = C + Cb
-  int tiles_m, tiles_n;
+  int tiles_m, tiles_n;      // tiles of (128*kCta) x 128
   int elem_bytes;            // 1: kind::f8f6f4, 2: kind::f16
   uint32_t fmt;              // idesc a/b format code
   uint32_t* flags;
@@ -74,6 +86,94 @@ OZ_DEVICE uint32_t ld_acquire_gpu(const uint32_t* p) {
 
 OZ_DEVICE void red_release_gpu_add(uint32_t* p, uint32_t v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ───────────── cluster / 2-CTA primitives ─────────────
+OZ_DEVICE uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+OZ_DEVICE void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Arrive on the mbarrier at the same smem offset in CTA `rank` of the cluster.
+OZ_DEVICE void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+// TMA load into this CTA's smem whose completion bytes land on the LEADER
+// CTA's barrier (peer bit cleared), as cta_group::2 MMAs require.
+OZ_DEVICE void tma_load_3d_pair(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                uint64_t cache_hint) {
+  const uint32_t leader_bar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2), "l"(cache_hint)
+      : "memory");
+}
+
+template <int kCta>
+OZ_DEVICE void tmem_alloc_g(uint32_t* dst) {
+  if constexpr (kCta == 1) {
+    tmem_alloc<kAccBufs * kPN>(dst);
+  } else {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
+                 "n"(kAccBufs * kPN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+}
+
+template <int kCta>
+OZ_DEVICE void tmem_dealloc_g(uint32_t taddr) {
+  if constexpr (kCta == 1)
+    tmem_dealloc<kAccBufs * kPN>(taddr);
+  else
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kAccBufs * kPN)
+                 : "memory");
+}
+
+// Commit all prior MMAs of this thread to `bar` (both CTAs' copies for kCta = 2).
+template <int kCta>
+OZ_DEVICE void mma_commit_g(uint64_t* bar) {
+  if constexpr (kCta == 1) {
+    mma_commit(bar);
+  } else {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)0x3)
+        : "memory");
+  }
+}
+
+template <int kCta>
+OZ_DEVICE void mma_issue(uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc, int elem_bytes) {
+  if constexpr (kCta == 1) {
+    if (elem_bytes == 1)
+      mma_f8f6f4(d_tmem, ad, bd, idesc, acc);
+    else
+      mma_f16(d_tmem, ad, bd, idesc, acc);
+  } else {
+    if (elem_bytes == 1)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+          "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+          "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+          : "memory");
+    else
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+          "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+          "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+          : "memory");
+  }
 }
 
 // Pair enumeration in reference order restricted to p < lp, q < lq, p+q <= cut.
@@ -119,18 +219,33 @@ OZ_DEVICE void tile_coords(int tile, int tiles_m, int tiles_n, int& tm, int& tn)
   tn = r / gm;
 }
 
-OZ_DEVICE void tile_limits(const PairParams& P, int tm, int tn, int& lp, int& lq) {
+// Pair limits for this CTA's 128-row slab (row128 = 128-row tile index).
+OZ_DEVICE void tile_limits(const PairParams& P, int row128, int tn, int& lp, int& lq) {
   lp = P.sx;
   lq = P.sy;
   if (P.tile_cnt_a) {
-    lp = min(lp, __ldg(P.tile_cnt_a + tm));
+    lp = row128 * kPM < P.m ? min(lp, __ldg(P.tile_cnt_a + row128)) : 0;
     lq = min(lq, __ldg(P.tile_cnt_b + tn));
+  }
+}
+
+// Limits of the pair sequence a tile-processing unit walks: for a CTA pair both
+// halves walk the same pairs (the wider A limit); a half whose rows have an
+// all-zero slice p simply adds nothing for it.
+template <int kCta>
+OZ_DEVICE void unit_limits(const PairParams& P, int tm, int tn, int& lp_walk, int& lq) {
+  tile_limits(P, tm * kCta, tn, lp_walk, lq);
+  if constexpr (kCta == 2) {
+    int lp1, lq1;
+    tile_limits(P, tm * kCta + 1, tn, lp1, lq1);
+    lp_walk = max(lp_walk, lp1);
   }
 }
 
 // T = ldexp(G, e) rebuilt from the FP32 bit pattern of a non-zero G (always a
 // normal FP32: a non-zero multiple of 2^(2(rho-53)) below 2^24).  Returns false
-// (and sets *zero) when the exact term underflows the reference's way.
+// when the term is not added: it underflowed to zero the reference's way (HW
+// mode) or left the normal range (flagged).
 OZ_DEVICE bool make_term(uint32_t g, int e, uint64_t& t, uint32_t& flags, bool emu) {
   const int ex = (int)((g >> 23) & 0xFFu) + (1023 - 127) + e;
   const uint64_t sign = (uint64_t)(g >> 31) << 63;
@@ -152,109 +267,120 @@ OZ_DEVICE bool make_term(uint32_t g, int e, uint64_t& t, uint32_t& flags, bool e
   return false;
 }
 
-template <bool kEmu>
+template <bool kEmu, int kCta>
 __global__ void __launch_bounds__(kPThreads, 1)
     pair_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const PairParams P) {
+  using Cfg = PairCfg<kCta>;
+  constexpr int kStages = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
-  PairSmem& s = *reinterpret_cast<PairSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  PairSmem<kCta>& s =
+      *reinterpret_cast<PairSmem<kCta>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x / 32;
   const int lane = (int)lane_id();
+  const uint32_t crank = kCta == 2 ? cluster_rank() : 0;  // rank in the CTA pair
+  const bool leader = crank == 0;
   const int num_tiles = P.tiles_m * P.tiles_n;
+  const int unit = blockIdx.x / kCta, num_units = gridDim.x / kCta;  // tile-processing unit (CTA or pair)
   const int kb_elems = 128 / P.elem_bytes;
   const int num_kb = (P.kb + kb_elems - 1) / kb_elems;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
-    for (int i = 0; i < kPStages; ++i) {
+    for (int i = 0; i < kStages; ++i) {
       mbar_init(&s.full[i], 1);
       mbar_init(&s.empty[i], 1);
     }
     for (int i = 0; i < kAccBufs; ++i) {
       mbar_init(&s.acc_full[i], 1);
-      mbar_init(&s.acc_empty[i], kEpiWarps);
+      mbar_init(&s.acc_empty[i], kEpiWarps * kCta);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<kAccBufs * kPN>(&s.tmem_base);
+  if (warp == 1) tmem_alloc_g<kCta>(&s.tmem_base);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kCta == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s.tmem_base;
 
   if (warp < 4) {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
-  if (warp == 0) {
-    // ───────── TMA producer ─────────
-    if (elect_one()) {
-      uint32_t it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if (warp == 0) {
+      // ───────── TMA producer (both CTAs of a pair load their own halves) ─────────
+      if (elect_one()) {
+        uint32_t it = 0;
+        for (int tile = unit; tile < num_tiles; tile += num_units) {
+          int tm, tn, lp, lq;
+          tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
+          unit_limits<kCta>(P, tm, tn, lp, lq);
+          const int wave = tile / num_units;
+          const int arow = (tm * kCta + (int)crank) * kPM;
+          const int brow = tn * kPN + (int)crank * Cfg::kBRows;
+          PairIter pi;
+          int t = 0;
+          for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++t) {
+            const int p = pi.p, q = pi.q();
+            if (P.step_ctr) {
+              // Wait until every CTA of the wave `pace_slack` steps back has issued its loads.
+              const int g = wave * P.pairs_per_tile + t - P.pace_slack;
+              if (g >= 0) {
+                const int gw = g / P.pairs_per_tile;
+                const uint32_t need = (uint32_t)(kCta * min(num_units, num_tiles - gw * num_units));
+                while (ld_acquire_gpu(P.step_ctr + g) < need) __nanosleep(32);
+              }
+            }
+            for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
+              const uint32_t st = it % kStages;
+              if (it >= (uint32_t)kStages) mbar_wait(&s.empty[st], ((it / kStages) - 1) & 1);
+              if constexpr (kCta == 1) {
+                mbar_arrive_expect_tx(&s.full[st], Cfg::kStageBytes);
+                tma_load_3d(s.a[st], &map_a, &s.full[st], kbi * kb_elems, arow, p, kEvictNormal);
+                tma_load_3d(s.b[st], &map_b, &s.full[st], kbi * kb_elems, brow, q, kEvictNormal);
+              } else {
+                if (leader) mbar_arrive_expect_tx(&s.full[st], 2 * Cfg::kStageBytes);
+                tma_load_3d_pair(s.a[st], &map_a, &s.full[st], kbi * kb_elems, arow, p, kEvictNormal);
+                tma_load_3d_pair(s.b[st], &map_b, &s.full[st], kbi * kb_elems, brow, q, kEvictNormal);
+              }
+            }
+            if (P.step_ctr) red_release_gpu_add(P.step_ctr + wave * P.pairs_per_tile + t, 1u);
+          }
+        }
+      }
+    } else if (warp == 1 && leader) {
+      // ───────── MMA issuer (leader CTA only) ─────────
+      const uint32_t idesc = make_idesc(P.fmt, P.fmt, kPM * kCta, kPN);
+      uint32_t it = 0, acc_it = 0;
+      for (int tile = unit; tile < num_tiles; tile += num_units) {
         int tm, tn, lp, lq;
         tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
-        tile_limits(P, tm, tn, lp, lq);
-        const int wave = tile / gridDim.x;
+        unit_limits<kCta>(P, tm, tn, lp, lq);
         PairIter pi;
-        int t = 0;
-        for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++t) {
-          const int p = pi.p, q = pi.q();
-          if (P.step_ctr) {
-            // Wait until every CTA of the wave `pace_slack` steps back has issued its loads.
-            const int g = wave * P.pairs_per_tile + t - P.pace_slack;
-            if (g >= 0) {
-              const int gw = g / P.pairs_per_tile;
-              const uint32_t need = (uint32_t)min((int)gridDim.x, num_tiles - gw * (int)gridDim.x);
-              while (ld_acquire_gpu(P.step_ctr + g) < need) __nanosleep(32);
-            }
-          }
-          for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
-            const uint32_t st = it % kPStages;
-            if (it >= (uint32_t)kPStages) mbar_wait(&s.empty[st], ((it / kPStages) - 1) & 1);
-            mbar_arrive_expect_tx(&s.full[st], kPStageBytes);
-            tma_load_3d(s.a[st], &map_a, &s.full[st], kbi * kb_elems, tm * kPM, p, kEvictNormal);
-            tma_load_3d(s.b[st], &map_b, &s.full[st], kbi * kb_elems, tn * kPN, q, kEvictNormal);
-          }
-          if (P.step_ctr) red_release_gpu_add(P.step_ctr + wave * P.pairs_per_tile + t, 1u);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ───────── MMA issuer ─────────
-    const uint32_t idesc = make_idesc(P.fmt, P.fmt, kPM, kPN);
-    uint32_t it = 0, acc_it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      int tm, tn, lp, lq;
-      tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
-      tile_limits(P, tm, tn, lp, lq);
-      PairIter pi;
-      for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
-        const uint32_t buf = acc_it % kAccBufs;
-        if (acc_it >= (uint32_t)kAccBufs) mbar_wait(&s.acc_empty[buf], ((acc_it / kAccBufs) - 1) & 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem + buf * kPN;
-        for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
-          const uint32_t st = it % kPStages;
-          mbar_wait(&s.full[st], (it / kPStages) & 1);
+        for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
+          const uint32_t buf = acc_it % kAccBufs;
+          if (acc_it >= (uint32_t)kAccBufs) mbar_wait(&s.acc_empty[buf], ((acc_it / kAccBufs) - 1) & 1);
           tc_fence_after();
-          if (elect_one()) {
-            const uint64_t ad = smem_desc_sw128(s.a[st]), bd = smem_desc_sw128(s.b[st]);
+          const uint32_t d_tmem = tmem + buf * kPN;
+          for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
+            const uint32_t st = it % kStages;
+            mbar_wait(&s.full[st], (it / kStages) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint64_t ad = smem_desc_sw128(s.a[st]), bd = smem_desc_sw128(s.b[st]);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const uint64_t off = (uint64_t)((kk * 32) >> 4);
-              if (P.elem_bytes == 1)
-                mma_f8f6f4(d_tmem, ad + off, bd + off, idesc, (kbi | kk) != 0);
-              else
-                mma_f16(d_tmem, ad + off, bd + off, idesc, (kbi | kk) != 0);
+              for (int kk = 0; kk < 4; ++kk) {
+                const uint64_t off = (uint64_t)((kk * 32) >> 4);
+                mma_issue<kCta>(d_tmem, ad + off, bd + off, idesc, (kbi | kk) != 0, P.elem_bytes);
+              }
+              mma_commit_g<kCta>(&s.empty[st]);
             }
-            mma_commit(&s.empty[st]);
+            __syncwarp();
           }
+          if (elect_one()) mma_commit_g<kCta>(&s.acc_full[buf]);
           __syncwarp();
         }
-        if (elect_one()) mma_commit(&s.acc_full[buf]);
-        __syncwarp();
       }
     }
-  }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
     // ───────── epilogue: ordered FP64 accumulation ─────────
@@ -263,11 +389,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const int epi_tid = threadIdx.x - 128;   // 0..255
     uint32_t flags = 0;
     uint32_t acc_it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int tile = unit; tile < num_tiles; tile += num_units) {
       int tm, tn, lp, lq;
       tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
-      tile_limits(P, tm, tn, lp, lq);
-      const int row = tm * kPM + quad * 32 + lane;
+      const int row128 = tm * kCta + (int)crank;
+      tile_limits(P, row128, tn, lp, lq);
+      int lp_walk;  // pairs the MMA issuer walks (unit_limits)
+      unit_limits<kCta>(P, tm, tn, lp_walk, lq);
+      const int row = row128 * kPM + quad * 32 + lane;
       const int col0 = tn * kPN + half * 64;
       // Stage the tile's B exponents (all planes we will touch) in smem.
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
@@ -285,34 +414,38 @@ __global__ void __launch_bounds__(kPThreads, 1)
       for (int j = 0; j < 64; ++j) cb[j] = Acc(0);
 
       PairIter pi;
-      for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
+      for (pi.init(lp_walk, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
         const int p = pi.p, q = pi.q();
-        const int ea = row < P.m ? __ldg(P.expo_a + (int64_t)p * P.m + row) : 0;
         const uint32_t buf = acc_it % kAccBufs;
         mbar_wait(&s.acc_full[buf], (acc_it / kAccBufs) & 1);
         tc_fence_after();
-        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + buf * kPN + half * 64;
+        // p >= lp: this CTA's rows have an all-zero A slice p (the partner needs it):
+        // the term is +0, nothing to add.
+        if (p < lp) {
+          const int ea = row < P.m ? __ldg(P.expo_a + (int64_t)p * P.m + row) : 0;
+          const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + buf * kPN + half * 64;
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t g[16];
-          tmem_ld16(taddr + ch * 16, g);
-          tmem_ld_wait();
-          const int4* ebv = reinterpret_cast<const int4*>(&s.eb[q][half * 64 + ch * 16]);
+          for (int ch = 0; ch < 4; ++ch) {
+            uint32_t g[16];
+            tmem_ld16(taddr + ch * 16, g);
+            tmem_ld_wait();
+            const int4* ebv = reinterpret_cast<const int4*>(&s.eb[q][half * 64 + ch * 16]);
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const int4 e4 = ebv[v];
-            const int eb4[4] = {e4.x, e4.y, e4.z, e4.w};
+            for (int v = 0; v < 4; ++v) {
+              const int4 e4 = ebv[v];
+              const int eb4[4] = {e4.x, e4.y, e4.z, e4.w};
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int j = ch * 16 + v * 4 + u;
-              const uint32_t gv = g[v * 4 + u];
-              if ((gv << 1) != 0u) {
-                uint64_t t;
-                if (make_term(gv, ea + eb4[u], t, flags, kEmu)) {
-                  if constexpr (kEmu)
-                    cb[j] = emu_add(cb[j], t, flags);
-                  else
-                    cb[j] = __dadd_rn(cb[j], u2d(t));
+              for (int u = 0; u < 4; ++u) {
+                const int j = ch * 16 + v * 4 + u;
+                const uint32_t gv = g[v * 4 + u];
+                if ((gv << 1) != 0u) {
+                  uint64_t t;
+                  if (make_term(gv, ea + eb4[u], t, flags, kEmu)) {
+                    if constexpr (kEmu)
+                      cb[j] = emu_add(cb[j], t, flags);
+                    else
+                      cb[j] = __dadd_rn(cb[j], u2d(t));
+                  }
                 }
               }
             }
@@ -320,7 +453,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&s.acc_empty[buf]);
+        if (lane == 0) {
+          if constexpr (kCta == 1) mbar_arrive(&s.acc_empty[buf]);
+          else mbar_arrive_cluster(&s.acc_empty[buf], 0);
+        }
       }
 
       // C = Cb (first block) or C = C + Cb (ozgemm.py:204-207).
@@ -368,15 +504,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<kAccBufs * kPN>(tmem);
+  if constexpr (kCta == 2) cluster_sync(); else __syncthreads();
+  if (warp == 1) tmem_dealloc_g<kCta>(tmem);
 }
 
-template __global__ void pair_gemm_kernel<false>(const __grid_constant__ CUtensorMap,
-                                                 const __grid_constant__ CUtensorMap, const PairParams);
-template __global__ void pair_gemm_kernel<true>(const __grid_constant__ CUtensorMap,
-                                                const __grid_constant__ CUtensorMap, const PairParams);
-
-size_t pair_gemm_smem_bytes() { return sizeof(PairSmem) + 1024; }
+template <int kCta>
+size_t pair_gemm_smem_bytes() {
+  return sizeof(PairSmem<kCta>) + 1024;
+}
 
 }  // namespace oz

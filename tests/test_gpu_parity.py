@@ -70,8 +70,11 @@ CASES = [
 @pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}x{c[1]}x{c[2]}-{c[4]}-{c[5]}-kb{c[6]}-emu{int(c[7])}"
                                              f"-ms{c[8]}-{c[9][:5]}-cut{c[10]}" for c in CASES])
 @pytest.mark.parametrize("skip", [True, False])
-def test_oz_gemm_bitwise(cuda, case, skip):
+@pytest.mark.parametrize("cta", ["1", "2"])
+def test_oz_gemm_bitwise(cuda, case, skip, cta, monkeypatch):
     import oracle
+
+    monkeypatch.setenv("OZ_CTA_GROUP", cta)  # read by oz_pair_gemm at each launch
 
     oz = _oz()
     m, n, k, phi, t2, t3, kbk, emu, ms, order, cut = case

@@ -1,0 +1,37 @@
+"""Arithmetic-throughput probes (DADD vs integer-emulated add vs int64 add vs FFMA)
+for choosing the fused epilogue's accumulation path.  Not part of the product."""
+import ctypes
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+SO = HERE / "libmicro.so"
+
+
+def build():
+    subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
+                    "-shared", "-Xcompiler", "-fPIC", "-o", str(SO), str(HERE / "microbench.cu")], check=True)
+
+
+def main(out=None):
+    if not SO.exists():
+        build()
+    lib = ctypes.CDLL(str(SO))
+    lib.micro_run.restype = ctypes.c_float
+    lib.micro_run.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    blocks, iters = 148 * 8, 4096
+    res = {}
+    for kind, name in enumerate(["dadd", "emu_add", "iadd64", "ffma"]):
+        ms = lib.micro_run(kind, blocks, iters)
+        ops = blocks * 256 * 16 * iters
+        res[name] = {"ms": ms, "Gops_per_s": ops / (ms / 1e3) / 1e9, "ops_per_clk_per_sm_at_1.9GHz":
+                     ops / (ms / 1e3) / 148 / 1.9e9}
+        print(name, json.dumps(res[name]))
+    if out:
+        Path(out).write_text(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else None)
