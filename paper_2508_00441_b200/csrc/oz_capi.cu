@@ -104,13 +104,12 @@ int launch_split(const oz::SplitParams& P, int emu, cudaStream_t st) {
   return launch_status();
 }
 
-template <bool kEmu, int kCta>
-int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const oz::PairParams& P, int units, cudaStream_t st) {
+template <bool kEmu, int kCta, int kEB>
+int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const oz::PairParams& P, int tiles, cudaStream_t st) {
   const size_t smem = oz::pair_gemm_smem_bytes<kCta>();
-  auto kern = oz::pair_gemm_kernel<kEmu, kCta>;
+  auto kern = oz::pair_gemm_kernel<kEmu, kCta, kEB>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(units * kCta));
   cfg.blockDim = dim3(oz::kPThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -121,12 +120,29 @@ int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const oz::PairPara
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // Persistent grid: never more units than can be co-resident (the pacing
+  // assumes every CTA of a wave runs concurrently).
+  int units = num_sms() / kCta;
+  cfg.gridDim = dim3((unsigned)(units * kCta));
+  int active = 0;
+  if (cudaOccupancyMaxActiveClusters(&active, kern, &cfg) == cudaSuccess && active > 0 && active < units)
+    units = active;
+  cudaGetLastError();
+  if (tiles < units) units = tiles;
+  cfg.gridDim = dim3((unsigned)(units * kCta));
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, P);
   if (e != cudaSuccess) {
     fprintf(stderr, "oz_b200: pair_gemm launch failed: %s\n", cudaGetErrorString(e));
     return OZ_ECUDA;
   }
   return launch_status();
+}
+
+template <bool kEmu, int kCta>
+int launch_pair_fmt(const CUtensorMap& ma, const CUtensorMap& mb, const oz::PairParams& P, int tiles,
+                    cudaStream_t st) {
+  return P.elem_bytes == 1 ? launch_pair<kEmu, kCta, 1>(ma, mb, P, tiles, st)
+                           : launch_pair<kEmu, kCta, 2>(ma, mb, P, tiles, st);
 }
 
 }  // namespace
@@ -225,6 +241,7 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   // 128-row slab; OZ_CTA_GROUP=1|2 overrides (experiments).
   int cta = m > oz::kPM ? 2 : 1;
   if (const char* e = getenv("OZ_CTA_GROUP")) cta = atoi(e) == 1 ? 1 : 2;
+  if (const char* e = getenv("OZ_DEBUG_MODE")) P.debug = atoi(e);
   CUtensorMap ma, mb;
   int rc = make_plane_map(&ma, a_planes, f.bytes, kb, m, planes_a, ld_a, oz::kPM);
   if (rc) return rc;
@@ -233,17 +250,15 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   P.tiles_m = (int)((m + oz::kPM * cta - 1) / (oz::kPM * cta));
   P.tiles_n = (int)((n + oz::kPN - 1) / oz::kPN);
   const int tiles = P.tiles_m * P.tiles_n;
-  const int units_max = num_sms() / cta;
-  const int units = tiles < units_max ? tiles : units_max;
   // Pacing needs an identical pair sequence in every tile (no skipping) and
-  // scratch counters (one per tile-wave and pair).
+  // scratch counters (one per tile-wave and pair); sized for the largest grid.
   P.step_ctr = nullptr; P.pace_slack = 0; P.pairs_per_tile = 0;
   if (!tile_cnt_a && pace_ws && pace_slack > 0) {
     int pairs = 0;
     for (int p = 0; p < sx; ++p)
       for (int q = 0; q < sy; ++q)
         if (pair_cutoff < 0 || p + q <= pair_cutoff) ++pairs;
-    const int waves = (tiles + units - 1) / units;
+    const int waves = tiles;  // upper bound: one unit
     const size_t need = sizeof(uint32_t) * (size_t)waves * (size_t)pairs;
     if (pairs > 0 && need <= (size_t)pace_ws_bytes) {
       cudaMemsetAsync(pace_ws, 0, need, st);
@@ -253,11 +268,11 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
     }
   }
   if (cta == 1) {
-    if (emu) return launch_pair<true, 1>(ma, mb, P, units, st);
-    return launch_pair<false, 1>(ma, mb, P, units, st);
+    if (emu) return launch_pair_fmt<true, 1>(ma, mb, P, tiles, st);
+    return launch_pair_fmt<false, 1>(ma, mb, P, tiles, st);
   }
-  if (emu) return launch_pair<true, 2>(ma, mb, P, units, st);
-  return launch_pair<false, 2>(ma, mb, P, units, st);
+  if (emu) return launch_pair_fmt<true, 2>(ma, mb, P, tiles, st);
+  return launch_pair_fmt<false, 2>(ma, mb, P, tiles, st);
 }
 
 int oz_dd_gemm(const double* A, const double* B, double* C, int64_t m, int64_t n, int64_t k, void* stream) {

@@ -76,6 +76,10 @@ struct PairParams {
   uint32_t* step_ctr;
   int pace_slack;
   int pairs_per_tile;
+  // Diagnostics only (OZ_DEBUG_MODE): bit 0 = epilogue skips TMEM loads/math,
+  // bit 1 = producer stops loading after the first ring fill (stale operands),
+  // bit 2 = MMA issuer ignores the stage barriers (pure issue rate).
+  int debug;
 };
 
 OZ_DEVICE uint32_t ld_acquire_gpu(const uint32_t* p) {
@@ -153,15 +157,17 @@ OZ_DEVICE void mma_commit_g(uint64_t* bar) {
   }
 }
 
-template <int kCta>
-OZ_DEVICE void mma_issue(uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc, int elem_bytes) {
+// One tcgen05.mma; the kind is a template parameter so no predicated-off
+// alternative instruction is emitted (those still occupy the tensor issue pipe).
+template <int kCta, int kElemBytes>
+OZ_DEVICE void mma_issue(uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
   if constexpr (kCta == 1) {
-    if (elem_bytes == 1)
+    if constexpr (kElemBytes == 1)
       mma_f8f6f4(d_tmem, ad, bd, idesc, acc);
     else
       mma_f16(d_tmem, ad, bd, idesc, acc);
   } else {
-    if (elem_bytes == 1)
+    if constexpr (kElemBytes == 1)
       asm volatile(
           "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
           "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
@@ -267,7 +273,7 @@ OZ_DEVICE bool make_term(uint32_t g, int e, uint64_t& t, uint32_t& flags, bool e
   return false;
 }
 
-template <bool kEmu, int kCta>
+template <bool kEmu, int kCta, int kElemBytes>
 __global__ void __launch_bounds__(kPThreads, 1)
     pair_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const PairParams P) {
@@ -282,7 +288,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const bool leader = crank == 0;
   const int num_tiles = P.tiles_m * P.tiles_n;
   const int unit = blockIdx.x / kCta, num_units = gridDim.x / kCta;  // tile-processing unit (CTA or pair)
-  const int kb_elems = 128 / P.elem_bytes;
+  constexpr int kb_elems = 128 / kElemBytes;
   const int num_kb = (P.kb + kb_elems - 1) / kb_elems;
 
   if (threadIdx.x == 0) {
@@ -310,6 +316,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       // ───────── TMA producer (both CTAs of a pair load their own halves) ─────────
       if (elect_one()) {
         uint32_t it = 0;
+        bool pacing = true;
         for (int tile = unit; tile < num_tiles; tile += num_units) {
           int tm, tn, lp, lq;
           tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
@@ -321,18 +328,31 @@ __global__ void __launch_bounds__(kPThreads, 1)
           int t = 0;
           for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++t) {
             const int p = pi.p, q = pi.q();
-            if (P.step_ctr) {
+            if (P.step_ctr && pacing) {
               // Wait until every CTA of the wave `pace_slack` steps back has issued its loads.
+              // Scheduling only: if that takes implausibly long (CTAs not co-resident),
+              // stop pacing instead of risking a deadlock.
               const int g = wave * P.pairs_per_tile + t - P.pace_slack;
               if (g >= 0) {
                 const int gw = g / P.pairs_per_tile;
                 const uint32_t need = (uint32_t)(kCta * min(num_units, num_tiles - gw * num_units));
-                while (ld_acquire_gpu(P.step_ctr + g) < need) __nanosleep(32);
+                const long long t0 = clock64();
+                while (ld_acquire_gpu(P.step_ctr + g) < need) {
+                  __nanosleep(32);
+                  if (clock64() - t0 > (1ll << 26)) {
+                    pacing = false;
+                    break;
+                  }
+                }
               }
             }
             for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
               const uint32_t st = it % kStages;
               if (it >= (uint32_t)kStages) mbar_wait(&s.empty[st], ((it / kStages) - 1) & 1);
+              if ((P.debug & 2) && it >= (uint32_t)kStages) {  // diagnostics: no memory traffic
+                if (leader) mbar_arrive(&s.full[st]);
+                continue;
+              }
               if constexpr (kCta == 1) {
                 mbar_arrive_expect_tx(&s.full[st], Cfg::kStageBytes);
                 tma_load_3d(s.a[st], &map_a, &s.full[st], kbi * kb_elems, arow, p, kEvictNormal);
@@ -363,14 +383,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
           const uint32_t d_tmem = tmem + buf * kPN;
           for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
             const uint32_t st = it % kStages;
-            mbar_wait(&s.full[st], (it / kStages) & 1);
+            if (!(P.debug & 4)) mbar_wait(&s.full[st], (it / kStages) & 1);  // bit 2: diagnostics, no waits
             tc_fence_after();
             if (elect_one()) {
               const uint64_t ad = smem_desc_sw128(s.a[st]), bd = smem_desc_sw128(s.b[st]);
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
                 const uint64_t off = (uint64_t)((kk * 32) >> 4);
-                mma_issue<kCta>(d_tmem, ad + off, bd + off, idesc, (kbi | kk) != 0, P.elem_bytes);
+                mma_issue<kCta, kElemBytes>(d_tmem, ad + off, bd + off, idesc, (kbi | kk) != 0);
               }
               mma_commit_g<kCta>(&s.empty[st]);
             }
@@ -421,7 +441,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         tc_fence_after();
         // p >= lp: this CTA's rows have an all-zero A slice p (the partner needs it):
         // the term is +0, nothing to add.
-        if (p < lp) {
+        if (p < lp && !(P.debug & 1)) {
           const int ea = row < P.m ? __ldg(P.expo_a + (int64_t)p * P.m + row) : 0;
           const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + buf * kPN + half * 64;
 #pragma unroll

@@ -203,8 +203,8 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True):
             _lib.call("oz_tile_counts", sb.row_cnt.data_ptr(), n, tcb.data_ptr(), sp)
         pace = None
         if tca is None and PACE_SLACK > 0 and m and n:
-            waves = -(-(((m + 127) // 128) * ((n + 127) // 128)) // _num_sms(torch))
-            pace = torch.empty(waves * max(kept, 1), dtype=torch.int32, device=A.device)
+            tiles = ((m + 127) // 128) * ((n + 127) // 128)  # upper bound on tile-waves
+            pace = torch.empty(tiles * max(kept, 1), dtype=torch.int32, device=A.device)
         _lib.call("oz_pair_gemm",
                   sa.planes.data_ptr() if sa.s else None, sb.planes.data_ptr() if sb.s else None,
                   sa.ld, sb.ld, sa.s, sb.s,

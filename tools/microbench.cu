@@ -53,3 +53,85 @@ extern "C" float micro_run(int kind, int blocks, int iters) {
   cudaFree(out);
   return ms;
 }
+
+// ───────── tcgen05 MMA throughput vs shape (operands resident in smem, SS mode) ─────────
+#include "../paper_2508_00441_b200/csrc/oz_pair_gemm.cu"
+
+template <int kCta, int kN>
+__global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long* cycles) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* a = base;                       // 128 rows x 128 B
+  uint8_t* b = base + 128 * 128;           // kN/kCta rows x 128 B
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x / 32;
+  for (int i = threadIdx.x; i < (128 + kN / kCta) * 128 / 4; i += blockDim.x) {
+    // random E4M3 slice-like bytes (|v| <= 1, no NaN): sign | exp 1..7 | mantissa
+    uint32_t h = (uint32_t)i * 2654435761u ^ (blockIdx.x * 97u);
+    uint32_t w = 0;
+    for (int b = 0; b < 4; ++b) { h = h * 1664525u + 1013904223u; w |= ((h >> 24) & 0xBFu) << (8 * b); }
+    reinterpret_cast<uint32_t*>(base)[i] = w;
+  }
+  if (threadIdx.x == 0) { oz::mbar_init(&bar[0], 1); oz::mbar_init(&bar[1], 1); oz::fence_barrier_init(); }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 0) oz::tmem_alloc_g<kCta>(&tbase);
+  oz::tc_fence_before();
+  if constexpr (kCta == 2) oz::cluster_sync(); else __syncthreads();
+  oz::tc_fence_after();
+  const bool leader = kCta == 1 || oz::cluster_rank() == 0;
+  if (warp == 0 && leader && oz::elect_one()) {
+    const uint32_t idesc = oz::make_idesc(0, 0, 128 * kCta, kN);
+    const uint64_t ad = oz::smem_desc_sw128(a), bd = oz::smem_desc_sw128(b);
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        oz::mma_issue<kCta>(tbase, ad + ((kk * 32) >> 4), bd + ((kk * 32) >> 4), idesc, 1u, 1);
+      oz::mma_commit_g<kCta>(&bar[it & 1]);
+      if (it >= 1) oz::mbar_wait(&bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
+    }
+    oz::mbar_wait(&bar[(iters - 1) & 1], ((iters - 1) >> 1) & 1);
+    cycles[blockIdx.x] = (unsigned long long)(clock64() - t0);
+  }
+  oz::tc_fence_before();
+  if constexpr (kCta == 2) oz::cluster_sync(); else __syncthreads();
+  if (warp == 0) oz::tmem_dealloc_g<kCta>(tbase);
+}
+
+template <int kCta, int kN>
+static double run_mma_rate(int iters) {
+  const int grid = 148;
+  unsigned long long* cyc;
+  cudaMalloc(&cyc, sizeof(unsigned long long) * grid);
+  cudaMemset(cyc, 0, sizeof(unsigned long long) * grid);
+  const size_t smem = (128 + kN) * 128 + 2048;
+  auto k = mma_rate<kCta, kN>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCta; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr; cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, iters, cyc);
+  cudaDeviceSynchronize();
+  unsigned long long h[148];
+  cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(cyc);
+  double mx = 0;
+  for (int i = 0; i < grid; ++i) mx = h[i] > mx ? (double)h[i] : mx;
+  // MACs per SM per cycle: each leader issues iters*4 MMAs of (128*kCta) x kN x 32 spread over kCta SMs
+  return (double)iters * 4 * 128 * kCta * kN * 32 / kCta / mx;
+}
+
+extern "C" double micro_mma_rate(int cta, int n, int iters) {
+  if (cta == 1 && n == 128) return run_mma_rate<1, 128>(iters);
+  if (cta == 1 && n == 256) return run_mma_rate<1, 256>(iters);
+  if (cta == 2 && n == 128) return run_mma_rate<2, 128>(iters);
+  if (cta == 2 && n == 192) return run_mma_rate<2, 192>(iters);
+  if (cta == 2 && n == 256) return run_mma_rate<2, 256>(iters);
+  return -1;
+}

@@ -29,6 +29,12 @@ def main(out=None):
         res[name] = {"ms": ms, "Gops_per_s": ops / (ms / 1e3) / 1e9, "ops_per_clk_per_sm_at_1.9GHz":
                      ops / (ms / 1e3) / 148 / 1.9e9}
         print(name, json.dumps(res[name]))
+    lib.micro_mma_rate.restype = ctypes.c_double
+    lib.micro_mma_rate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    for cta, n in ((1, 128), (1, 256), (2, 128), (2, 192), (2, 256)):
+        r = lib.micro_mma_rate(cta, n, 20000)
+        res[f"mma_fp8_cta{cta}_n{n}"] = {"macs_per_clk_per_sm": r, "frac_of_8192": r / 8192}
+        print(f"mma fp8 cta_group::{cta} N={n}: {r:.0f} MAC/clk/SM ({r / 8192:.2f} of 8192)", flush=True)
     if out:
         Path(out).write_text(json.dumps(res, indent=1))
 
