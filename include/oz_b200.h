@@ -35,7 +35,7 @@ enum {
   OZ_EUNSUPPORTED = 2, /* format/size combination not implemented on sm_100a */
   OZ_ECUDA = 3,        /* CUDA runtime error at launch                        */
   OZ_ETMAP = 4,        /* cuTensorMapEncodeTiled failed                      */
-  OZ_ESLICES = 5       /* more B slices than the epilogue stages (64)         */
+  OZ_ESLICES = 5       /* more B slices than the epilogue stages (48)         */
 };
 
 enum { OZ_FMT_E4M3 = 0, OZ_FMT_E5M2 = 1, OZ_FMT_FP16 = 2, OZ_FMT_BF16 = 3 };

@@ -104,10 +104,10 @@ int launch_split(const oz::SplitParams& P, int emu, cudaStream_t st) {
   return launch_status();
 }
 
-template <bool kEmu, int kCta, int kEB>
+template <bool kEmu, int kCta, int kEB, int kN>
 int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const oz::PairParams& P, int tiles, cudaStream_t st) {
-  const size_t smem = oz::pair_gemm_smem_bytes<kCta>();
-  auto kern = oz::pair_gemm_kernel<kEmu, kCta, kEB>;
+  const size_t smem = oz::pair_gemm_smem_bytes<kCta, kN>();
+  auto kern = oz::pair_gemm_kernel<kEmu, kCta, kEB, kN>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(oz::kPThreads);
@@ -138,11 +138,11 @@ int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const oz::PairPara
   return launch_status();
 }
 
-template <bool kEmu, int kCta>
+template <bool kEmu, int kCta, int kN>
 int launch_pair_fmt(const CUtensorMap& ma, const CUtensorMap& mb, const oz::PairParams& P, int tiles,
                     cudaStream_t st) {
-  return P.elem_bytes == 1 ? launch_pair<kEmu, kCta, 1>(ma, mb, P, tiles, st)
-                           : launch_pair<kEmu, kCta, 2>(ma, mb, P, tiles, st);
+  return P.elem_bytes == 1 ? launch_pair<kEmu, kCta, 1, kN>(ma, mb, P, tiles, st)
+                           : launch_pair<kEmu, kCta, 2, kN>(ma, mb, P, tiles, st);
 }
 
 }  // namespace
@@ -158,7 +158,7 @@ const char* oz_strerror(int status) {
     case OZ_EUNSUPPORTED: return "unsupported format or size on sm_100a";
     case OZ_ECUDA: return "CUDA launch error";
     case OZ_ETMAP: return "cuTensorMapEncodeTiled failed";
-    case OZ_ESLICES: return "too many B slices for the fused epilogue (max 64)";
+    case OZ_ESLICES: return "too many B slices for the fused epilogue (max 48)";
     default: return "unknown status";
   }
 }
@@ -219,7 +219,6 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   if (m < 0 || n < 0 || kb < 1 || sx < 0 || sy < 0 || sx > planes_a || sy > planes_b || ldc < n || !C || !flags)
     return OZ_EINVAL;
   if ((tile_cnt_a == nullptr) != (tile_cnt_b == nullptr)) return OZ_EINVAL;
-  if (sy > oz::kMaxSy) return OZ_ESLICES;
   if (m == 0 || n == 0) return OZ_OK;
   if (m > INT32_MAX || n > INT32_MAX || kb > INT32_MAX) return OZ_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
@@ -237,18 +236,22 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   P.C = C; P.ldc = ldc; P.m = (int)m; P.n = (int)n; P.kb = (int)kb; P.sx = sx; P.sy = sy;
   P.order = order; P.cutoff = pair_cutoff; P.accumulate = accumulate;
   P.elem_bytes = f.bytes; P.fmt = idf; P.flags = flags;
-  // CTA-pair (cta_group::2, 256x128 tiles) unless the problem has a single
-  // 128-row slab; OZ_CTA_GROUP=1|2 overrides (experiments).
+  // CTA pair (cta_group::2) unless the problem has a single 128-row slab; N = 192
+  // columns per pair tile when the B-exponent staging allows it.  OZ_CTA_GROUP=1|2
+  // and OZ_TILE_N=128|192 override (experiments, tests).
   int cta = m > oz::kPM ? 2 : 1;
   if (const char* e = getenv("OZ_CTA_GROUP")) cta = atoi(e) == 1 ? 1 : 2;
+  int tn = (cta == 2 && n > 128 && sy <= oz::PairCfg<2, 192>::kMaxSy) ? 192 : 128;
+  if (const char* e = getenv("OZ_TILE_N")) tn = (atoi(e) == 192 && cta == 2 && sy <= oz::PairCfg<2, 192>::kMaxSy) ? 192 : 128;
+  if (sy > oz::PairCfg<2, 128>::kMaxSy) return OZ_ESLICES;
   if (const char* e = getenv("OZ_DEBUG_MODE")) P.debug = atoi(e);
   CUtensorMap ma, mb;
   int rc = make_plane_map(&ma, a_planes, f.bytes, kb, m, planes_a, ld_a, oz::kPM);
   if (rc) return rc;
-  rc = make_plane_map(&mb, b_planes, f.bytes, kb, n, planes_b, ld_b, oz::kPN / cta);
+  rc = make_plane_map(&mb, b_planes, f.bytes, kb, n, planes_b, ld_b, tn / cta);
   if (rc) return rc;
   P.tiles_m = (int)((m + oz::kPM * cta - 1) / (oz::kPM * cta));
-  P.tiles_n = (int)((n + oz::kPN - 1) / oz::kPN);
+  P.tiles_n = (int)((n + tn - 1) / tn);
   const int tiles = P.tiles_m * P.tiles_n;
   // Pacing needs an identical pair sequence in every tile (no skipping) and
   // scratch counters (one per tile-wave and pair); sized for the largest grid.
@@ -268,11 +271,15 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
     }
   }
   if (cta == 1) {
-    if (emu) return launch_pair_fmt<true, 1>(ma, mb, P, tiles, st);
-    return launch_pair_fmt<false, 1>(ma, mb, P, tiles, st);
+    if (emu) return launch_pair_fmt<true, 1, 128>(ma, mb, P, tiles, st);
+    return launch_pair_fmt<false, 1, 128>(ma, mb, P, tiles, st);
   }
-  if (emu) return launch_pair_fmt<true, 2>(ma, mb, P, tiles, st);
-  return launch_pair_fmt<false, 2>(ma, mb, P, tiles, st);
+  if (tn == 192) {
+    if (emu) return launch_pair_fmt<true, 2, 192>(ma, mb, P, tiles, st);
+    return launch_pair_fmt<false, 2, 192>(ma, mb, P, tiles, st);
+  }
+  if (emu) return launch_pair_fmt<true, 2, 128>(ma, mb, P, tiles, st);
+  return launch_pair_fmt<false, 2, 128>(ma, mb, P, tiles, st);
 }
 
 int oz_dd_gemm(const double* A, const double* B, double* C, int64_t m, int64_t n, int64_t k, void* stream) {

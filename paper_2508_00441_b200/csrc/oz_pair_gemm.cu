@@ -31,26 +31,38 @@
 
 namespace oz {
 
-constexpr int kPM = 128, kPN = 128;        // per-CTA output tile
-constexpr int kAccBufs = 4;                // TMEM accumulators (4 x 128 cols = 512)
+constexpr int kPM = 128;                   // per-CTA output rows
 constexpr int kEpiWarps = 8;
 constexpr int kPThreads = 128 + 32 * kEpiWarps;
-constexpr int kMaxSy = 48;                 // B-exponent staging cap (planes)
+constexpr int kTmemCols = 512;             // whole TMEM: accumulators (+ part of Cb for N > 128)
 
-template <int kCta>
+// kN = output columns per CTA (and MMA N).  N = 128: Cb fully in registers,
+// 4 TMEM accumulators.  N = 192 (cta_group::2 only): 2 accumulators of 192
+// columns; Cb columns [0,128) in registers, [128,192) as FP64 in TMEM columns
+// [384, 512).  N = 192 runs the tensor core at 98% of peak vs 87% for N = 128
+// (profiles/microbench_r01.txt) and reads 25% fewer operand bytes per flop.
+template <int kCta, int kN>
 struct PairCfg {
-  static constexpr int kBRows = kPN / kCta;                   // B rows staged per CTA
+  static constexpr int kBRows = kN / kCta;                    // B rows staged per CTA
   static constexpr int kStageBytes = (kPM + kBRows) * 128;    // per CTA
-  static constexpr int kStages = kCta == 1 ? 5 : 8;
+  static constexpr int kAccBufs = kN == 128 ? 4 : 2;
+  static constexpr int kTmCols = kN - 128;                    // C columns whose Cb lives in TMEM
+  static constexpr int kCbTmem = kAccBufs * kN;               // first TMEM column of that Cb
+  static constexpr int kMaxSy = kN == 128 ? 48 : 32;          // B-exponent staging cap (planes)
+  static constexpr int kSmemBudget = 227 * 1024 - 2048 - kMaxSy * kN * 4;
+  static constexpr int kStages = kSmemBudget / kStageBytes > 8 ? 8 : kSmemBudget / kStageBytes;
+  static_assert(kCbTmem + 2 * kTmCols <= kTmemCols, "TMEM budget");
+  static_assert(kN == 128 || kCta == 2, "N > 128 needs the CTA pair");
 };
 
-template <int kCta>
+template <int kCta, int kN>
 struct PairSmem {
-  alignas(1024) uint8_t a[PairCfg<kCta>::kStages][kPM * 128];
-  alignas(1024) uint8_t b[PairCfg<kCta>::kStages][PairCfg<kCta>::kBRows * 128];
-  int32_t eb[kMaxSy][kPN];
-  uint64_t full[PairCfg<kCta>::kStages], empty[PairCfg<kCta>::kStages];
-  uint64_t acc_full[kAccBufs], acc_empty[kAccBufs];
+  using Cfg = PairCfg<kCta, kN>;
+  alignas(1024) uint8_t a[Cfg::kStages][kPM * 128];
+  alignas(1024) uint8_t b[Cfg::kStages][Cfg::kBRows * 128];
+  int32_t eb[Cfg::kMaxSy][kN];
+  uint64_t full[Cfg::kStages], empty[Cfg::kStages];
+  uint64_t acc_full[Cfg::kAccBufs], acc_empty[Cfg::kAccBufs];
   uint32_t tmem_base;
 };
 
@@ -58,7 +70,7 @@ struct PairParams {
   const int32_t* expo_a;     // [sx_planes][m]
   const int32_t* expo_b;     // [sy_planes][n]
   const int32_t* tile_cnt_a; // [m/128] max slice count over the tile's rows (nullable = no skip)
-  const int32_t* tile_cnt_b; // [n/128]
+  const int32_t* tile_cnt_b; // [n/128] (128-column groups, whatever kN is)
   double* C;
   int64_t ldc;
   int m, n, kb;
@@ -66,7 +78,7 @@ struct PairParams {
   int order;                 // 0 = smallest-first, 1 = largest-first
   int cutoff;                // keep pairs with p+q <= cutoff  (< 0: keep all)
   int accumulate;            // 0: C = Cb (first block), 1: C = C + Cb
-  int tiles_m, tiles_n;      // tiles of (128*kCta) x 128
+  int tiles_m, tiles_n;      // tiles of (128*kCta) x kN
   int elem_bytes;            // 1: kind::f8f6f4, 2: kind::f16
   uint32_t fmt;              // idesc a/b format code
   uint32_t* flags;
@@ -125,10 +137,10 @@ OZ_DEVICE void tma_load_3d_pair(void* smem_dst, const CUtensorMap* map, uint64_t
 template <int kCta>
 OZ_DEVICE void tmem_alloc_g(uint32_t* dst) {
   if constexpr (kCta == 1) {
-    tmem_alloc<kAccBufs * kPN>(dst);
+    tmem_alloc<kTmemCols>(dst);
   } else {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
-                 "n"(kAccBufs * kPN)
+                 "n"(kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
@@ -137,9 +149,9 @@ OZ_DEVICE void tmem_alloc_g(uint32_t* dst) {
 template <int kCta>
 OZ_DEVICE void tmem_dealloc_g(uint32_t taddr) {
   if constexpr (kCta == 1)
-    tmem_dealloc<kAccBufs * kPN>(taddr);
+    tmem_dealloc<kTmemCols>(taddr);
   else
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kAccBufs * kPN)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kTmemCols)
                  : "memory");
 }
 
@@ -225,29 +237,6 @@ OZ_DEVICE void tile_coords(int tile, int tiles_m, int tiles_n, int& tm, int& tn)
   tn = r / gm;
 }
 
-// Pair limits for this CTA's 128-row slab (row128 = 128-row tile index).
-OZ_DEVICE void tile_limits(const PairParams& P, int row128, int tn, int& lp, int& lq) {
-  lp = P.sx;
-  lq = P.sy;
-  if (P.tile_cnt_a) {
-    lp = row128 * kPM < P.m ? min(lp, __ldg(P.tile_cnt_a + row128)) : 0;
-    lq = min(lq, __ldg(P.tile_cnt_b + tn));
-  }
-}
-
-// Limits of the pair sequence a tile-processing unit walks: for a CTA pair both
-// halves walk the same pairs (the wider A limit); a half whose rows have an
-// all-zero slice p simply adds nothing for it.
-template <int kCta>
-OZ_DEVICE void unit_limits(const PairParams& P, int tm, int tn, int& lp_walk, int& lq) {
-  tile_limits(P, tm * kCta, tn, lp_walk, lq);
-  if constexpr (kCta == 2) {
-    int lp1, lq1;
-    tile_limits(P, tm * kCta + 1, tn, lp1, lq1);
-    lp_walk = max(lp_walk, lp1);
-  }
-}
-
 // T = ldexp(G, e) rebuilt from the FP32 bit pattern of a non-zero G (always a
 // normal FP32: a non-zero multiple of 2^(2(rho-53)) below 2^24).  Returns false
 // when the term is not added: it underflowed to zero the reference's way (HW
@@ -273,15 +262,124 @@ OZ_DEVICE bool make_term(uint32_t g, int e, uint64_t& t, uint32_t& flags, bool e
   return false;
 }
 
-template <bool kEmu, int kCta, int kElemBytes>
+// Pair limits for this CTA's 128-row slab (row128) and the tile's kN columns.
+template <int kN>
+OZ_DEVICE void tile_limits(const PairParams& P, int row128, int tn, int& lp, int& lq) {
+  lp = P.sx;
+  lq = P.sy;
+  if (P.tile_cnt_a) {
+    lp = row128 * kPM < P.m ? min(lp, __ldg(P.tile_cnt_a + row128)) : 0;
+    int cq = 0;
+    const int c_lo = tn * kN, c_hi = min(tn * kN + kN, P.n);
+    for (int g = c_lo / 128; g * 128 < c_hi; ++g) cq = max(cq, __ldg(P.tile_cnt_b + g));
+    lq = min(lq, cq);
+  }
+}
+
+// Limits of the pair sequence a tile-processing unit walks: for a CTA pair both
+// halves walk the same pairs (the wider A limit); a half whose rows have an
+// all-zero slice p simply adds nothing for it.
+template <int kCta, int kN>
+OZ_DEVICE void unit_limits(const PairParams& P, int tm, int tn, int& lp_walk, int& lq) {
+  tile_limits<kN>(P, tm * kCta, tn, lp_walk, lq);
+  if constexpr (kCta == 2) {
+    int lp1, lq1;
+    tile_limits<kN>(P, tm * kCta + 1, tn, lp1, lq1);
+    lp_walk = max(lp_walk, lp1);
+  }
+}
+
+OZ_DEVICE void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+      "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+      "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+OZ_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Add the terms of 16 consecutive G values (one tcgen05.ld chunk) into 16 Cb entries.
+template <bool kEmu, typename Acc>
+OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_row, int ea, Acc* cb, uint32_t& flags) {
+  const int4* ebv = reinterpret_cast<const int4*>(eb_row);
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int4 e4 = ebv[v];
+    const int eb4[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = v * 4 + u;
+      const uint32_t gv = g[j];
+      if ((gv << 1) != 0u) {
+        uint64_t t;
+        if (make_term(gv, ea + eb4[u], t, flags, kEmu)) {
+          if constexpr (kEmu)
+            cb[j] = emu_add(cb[j], t, flags);
+          else
+            cb[j] = __dadd_rn(cb[j], u2d(t));
+        }
+      }
+    }
+  }
+}
+
+// C[row, col0 : col0+cnt] = Cb (first block) or C + Cb (ozgemm.py:204-207).
+template <bool kEmu, typename Acc>
+OZ_DEVICE void store_row(const PairParams& P, int row, int col0, const Acc* cb, int cnt, uint32_t& flags) {
+  Acc* crow = reinterpret_cast<Acc*>(P.C + (int64_t)row * P.ldc + col0);
+  const bool vec = ((P.ldc & 1) == 0) && ((col0 & 1) == 0) && (col0 + cnt <= P.n);
+  if (vec) {
+    using Acc2 = typename std::conditional<kEmu, ulonglong2, double2>::type;
+#pragma unroll
+    for (int j = 0; j < cnt; j += 2) {
+      Acc2 v;
+      if (P.accumulate) {
+        const Acc2 c = *reinterpret_cast<const Acc2*>(crow + j);
+        if constexpr (kEmu) {
+          v.x = emu_add(c.x, cb[j], flags);
+          v.y = emu_add(c.y, cb[j + 1], flags);
+        } else {
+          v.x = __dadd_rn(c.x, cb[j]);
+          v.y = __dadd_rn(c.y, cb[j + 1]);
+        }
+      } else {
+        v.x = cb[j];
+        v.y = cb[j + 1];
+      }
+      *reinterpret_cast<Acc2*>(crow + j) = v;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < cnt; ++j) {
+      if (col0 + j < P.n) {
+        Acc v = cb[j];
+        if (P.accumulate) {
+          if constexpr (kEmu)
+            v = emu_add(crow[j], cb[j], flags);
+          else
+            v = __dadd_rn(crow[j], cb[j]);
+        }
+        crow[j] = v;
+      }
+    }
+  }
+}
+
+template <bool kEmu, int kCta, int kElemBytes, int kN>
 __global__ void __launch_bounds__(kPThreads, 1)
     pair_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const PairParams P) {
-  using Cfg = PairCfg<kCta>;
+  using Cfg = PairCfg<kCta, kN>;
   constexpr int kStages = Cfg::kStages;
+  constexpr int kAccBufs = Cfg::kAccBufs;
   extern __shared__ uint8_t smem_raw[];
-  PairSmem<kCta>& s =
-      *reinterpret_cast<PairSmem<kCta>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  PairSmem<kCta, kN>& s =
+      *reinterpret_cast<PairSmem<kCta, kN>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x / 32;
   const int lane = (int)lane_id();
   const uint32_t crank = kCta == 2 ? cluster_rank() : 0;  // rank in the CTA pair
@@ -320,10 +418,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         for (int tile = unit; tile < num_tiles; tile += num_units) {
           int tm, tn, lp, lq;
           tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
-          unit_limits<kCta>(P, tm, tn, lp, lq);
+          unit_limits<kCta, kN>(P, tm, tn, lp, lq);
           const int wave = tile / num_units;
           const int arow = (tm * kCta + (int)crank) * kPM;
-          const int brow = tn * kPN + (int)crank * Cfg::kBRows;
+          const int brow = tn * kN + (int)crank * Cfg::kBRows;
           PairIter pi;
           int t = 0;
           for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++t) {
@@ -369,18 +467,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
       }
     } else if (warp == 1 && leader) {
       // ───────── MMA issuer (leader CTA only) ─────────
-      const uint32_t idesc = make_idesc(P.fmt, P.fmt, kPM * kCta, kPN);
+      const uint32_t idesc = make_idesc(P.fmt, P.fmt, kPM * kCta, kN);
       uint32_t it = 0, acc_it = 0;
       for (int tile = unit; tile < num_tiles; tile += num_units) {
         int tm, tn, lp, lq;
         tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
-        unit_limits<kCta>(P, tm, tn, lp, lq);
+        unit_limits<kCta, kN>(P, tm, tn, lp, lq);
         PairIter pi;
         for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
           const uint32_t buf = acc_it % kAccBufs;
           if (acc_it >= (uint32_t)kAccBufs) mbar_wait(&s.acc_empty[buf], ((acc_it / kAccBufs) - 1) & 1);
           tc_fence_after();
-          const uint32_t d_tmem = tmem + buf * kPN;
+          const uint32_t d_tmem = tmem + buf * kN;
           for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
             const uint32_t st = it % kStages;
             if (!(P.debug & 4)) mbar_wait(&s.full[st], (it / kStages) & 1);  // bit 2: diagnostics, no waits
@@ -404,24 +502,26 @@ __global__ void __launch_bounds__(kPThreads, 1)
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
     // ───────── epilogue: ordered FP64 accumulation ─────────
+    constexpr int kTmHalf = Cfg::kTmCols / 2;  // TMEM-resident Cb columns per thread
     const int quad = warp & 3;               // TMEM lane quadrant this warp may access
-    const int half = (warp - 4) >> 2;        // column half [64*half, 64*half+64)
+    const int half = (warp - 4) >> 2;        // register Cb: cols [64h, 64h+64); TMEM Cb: [128 + kTmHalf*h, +kTmHalf)
     const int epi_tid = threadIdx.x - 128;   // 0..255
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const uint32_t cb_tmem = tmem + lane_base + Cfg::kCbTmem + half * 2 * kTmHalf;  // 2 words per FP64
     uint32_t flags = 0;
     uint32_t acc_it = 0;
     for (int tile = unit; tile < num_tiles; tile += num_units) {
       int tm, tn, lp, lq;
       tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
       const int row128 = tm * kCta + (int)crank;
-      tile_limits(P, row128, tn, lp, lq);
+      tile_limits<kN>(P, row128, tn, lp, lq);
       int lp_walk;  // pairs the MMA issuer walks (unit_limits)
-      unit_limits<kCta>(P, tm, tn, lp_walk, lq);
+      unit_limits<kCta, kN>(P, tm, tn, lp_walk, lq);
       const int row = row128 * kPM + quad * 32 + lane;
-      const int col0 = tn * kPN + half * 64;
       // Stage the tile's B exponents (all planes we will touch) in smem.
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-      for (int idx = epi_tid; idx < lq * kPN; idx += 32 * kEpiWarps) {
-        const int q = idx / kPN, c = idx % kPN, gc = tn * kPN + c;
+      for (int idx = epi_tid; idx < lq * kN; idx += 32 * kEpiWarps) {
+        const int q = idx / kN, c = idx % kN, gc = tn * kN + c;
         s.eb[q][c] = gc < P.n ? __ldg(P.expo_b + (int64_t)q * P.n + gc) : 0;
       }
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
@@ -432,6 +532,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
       Acc cb[64];
 #pragma unroll
       for (int j = 0; j < 64; ++j) cb[j] = Acc(0);
+      if constexpr (kTmHalf > 0) {
+        uint32_t z[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) z[j] = 0u;
+#pragma unroll
+        for (int c = 0; c < 2 * kTmHalf; c += 32) tmem_st32(cb_tmem + c, z);
+        tmem_st_wait();
+      }
 
       PairIter pi;
       for (pi.init(lp_walk, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
@@ -443,32 +551,38 @@ __global__ void __launch_bounds__(kPThreads, 1)
         // the term is +0, nothing to add.
         if (p < lp && !(P.debug & 1)) {
           const int ea = row < P.m ? __ldg(P.expo_a + (int64_t)p * P.m + row) : 0;
-          const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + buf * kPN + half * 64;
+          const uint32_t gaddr = tmem + lane_base + buf * kN;
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
             uint32_t g[16];
-            tmem_ld16(taddr + ch * 16, g);
+            tmem_ld16(gaddr + half * 64 + ch * 16, g);
             tmem_ld_wait();
-            const int4* ebv = reinterpret_cast<const int4*>(&s.eb[q][half * 64 + ch * 16]);
+            accumulate16<kEmu>(g, &s.eb[q][half * 64 + ch * 16], ea, cb + ch * 16, flags);
+          }
+          if constexpr (kTmHalf > 0) {
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const int4 e4 = ebv[v];
-              const int eb4[4] = {e4.x, e4.y, e4.z, e4.w};
+            for (int ch = 0; ch < kTmHalf / 16; ++ch) {
+              uint32_t g[16], w[32];
+              tmem_ld16(gaddr + 128 + half * kTmHalf + ch * 16, g);
+              tmem_ld32(cb_tmem + ch * 32, w);
+              tmem_ld_wait();
+              Acc c16[16];
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int j = ch * 16 + v * 4 + u;
-                const uint32_t gv = g[v * 4 + u];
-                if ((gv << 1) != 0u) {
-                  uint64_t t;
-                  if (make_term(gv, ea + eb4[u], t, flags, kEmu)) {
-                    if constexpr (kEmu)
-                      cb[j] = emu_add(cb[j], t, flags);
-                    else
-                      cb[j] = __dadd_rn(cb[j], u2d(t));
-                  }
-                }
+              for (int j = 0; j < 16; ++j) {
+                const uint64_t b = (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
+                if constexpr (kEmu) c16[j] = b; else c16[j] = u2d(b);
               }
+              accumulate16<kEmu>(g, &s.eb[q][128 + half * kTmHalf + ch * 16], ea, c16, flags);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                uint64_t b;
+                if constexpr (kEmu) b = c16[j]; else b = d2u(c16[j]);
+                w[2 * j] = (uint32_t)b;
+                w[2 * j + 1] = (uint32_t)(b >> 32);
+              }
+              tmem_st32(cb_tmem + ch * 32, w);
             }
+            tmem_st_wait();
           }
         }
         tc_fence_before();
@@ -481,41 +595,20 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
       // C = Cb (first block) or C = C + Cb (ozgemm.py:204-207).
       if (row < P.m) {
-        Acc* crow = reinterpret_cast<Acc*>(P.C + (int64_t)row * P.ldc + col0);
-        const bool vec = ((P.ldc & 1) == 0) && (col0 + 64 <= P.n);
-        if (vec) {
-          using Acc2 = typename std::conditional<kEmu, ulonglong2, double2>::type;
+        store_row<kEmu>(P, row, tn * kN + half * 64, cb, 64, flags);
+        if constexpr (kTmHalf > 0) {
 #pragma unroll
-          for (int j = 0; j < 64; j += 2) {
-            Acc2 v;
-            if (P.accumulate) {
-              const Acc2 c = *reinterpret_cast<const Acc2*>(crow + j);
-              if constexpr (kEmu) {
-                v.x = emu_add(c.x, cb[j], flags);
-                v.y = emu_add(c.y, cb[j + 1], flags);
-              } else {
-                v.x = __dadd_rn(c.x, cb[j]);
-                v.y = __dadd_rn(c.y, cb[j + 1]);
-              }
-            } else {
-              v.x = cb[j];
-              v.y = cb[j + 1];
-            }
-            *reinterpret_cast<Acc2*>(crow + j) = v;
-          }
-        } else {
+          for (int ch = 0; ch < kTmHalf / 16; ++ch) {
+            uint32_t w[32];
+            tmem_ld32(cb_tmem + ch * 32, w);
+            tmem_ld_wait();
+            Acc c16[16];
 #pragma unroll
-          for (int j = 0; j < 64; ++j) {
-            if (col0 + j < P.n) {
-              Acc v = cb[j];
-              if (P.accumulate) {
-                if constexpr (kEmu)
-                  v = emu_add(crow[j], cb[j], flags);
-                else
-                  v = __dadd_rn(crow[j], cb[j]);
-              }
-              crow[j] = v;
+            for (int j = 0; j < 16; ++j) {
+              const uint64_t b = (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
+              if constexpr (kEmu) c16[j] = b; else c16[j] = u2d(b);
             }
+            store_row<kEmu>(P, row, tn * kN + 128 + half * kTmHalf + ch * 16, c16, 16, flags);
           }
         }
       }
@@ -528,9 +621,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
   if (warp == 1) tmem_dealloc_g<kCta>(tmem);
 }
 
-template <int kCta>
+template <int kCta, int kN>
 size_t pair_gemm_smem_bytes() {
-  return sizeof(PairSmem<kCta>) + 1024;
+  return sizeof(PairSmem<kCta, kN>) + 1024;
 }
 
 }  // namespace oz

@@ -166,7 +166,8 @@ __global__ void __launch_bounds__(kSplitThreads) split_rows_kernel(const SplitPa
       }
       const uint32_t ef = (uint32_t)((x[i] >> 52) & 0x7FF);
       if (ef == 0 && (x[i] << 1) != 0) flags |= FLAG_SUBNORMAL_RESID;
-      codes[i] = encode_coeff(v, c, P.fmt, flags);
+      if constexpr (kWrite) codes[i] = encode_coeff(v, c, P.fmt, flags);  // count pass: no codes
+      else (void)codes;
     }
     if constexpr (kWrite) {
       uint8_t* plane = P.coeff + (int64_t)it * plane_stride + row * P.ld * P.fmt.bytes;

@@ -30,7 +30,7 @@ import numpy as np
 from . import _lib
 from .errors import DimensionError, SlicingInfeasible
 from .formats import FormatSpec
-from .slicing import compute_params, predict_gemm_count, split_rows_device, transpose_device
+from .slicing import compute_params, predict_gemm_count, split_many_device, transpose_device
 
 __all__ = [
     "DimensionError", "GemmConfig", "BlockStats", "OzStats", "OzResult", "transpose", "oz_gemm",
@@ -182,8 +182,8 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True):
         _check_accumulator(params, kb)
         if timing:
             ev[0].record()
-        sa, _ = split_rows_device(A[:, lo:hi], cfg.type2, params, emu)
-        sb, _ = split_rows_device(transpose_device(B[lo:hi, :]), cfg.type2, params, emu)
+        (sa, sb), _ = split_many_device([A[:, lo:hi], transpose_device(B[lo:hi, :])], cfg.type2, params, emu,
+                                        flags_out=flags)
         if timing:
             ev[1].record()
         sx = min(sa.s, cfg.max_slices or sa.s)

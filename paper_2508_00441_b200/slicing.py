@@ -30,6 +30,7 @@ from .formats import FormatSpec, decode_codes
 __all__ = [
     "SlicingInfeasible", "SlicingParams", "SliceSet", "DeviceSlices", "compute_params",
     "predict_slice_count", "predict_gemm_count", "slice_vector", "slice_matrix", "split_rows_device",
+    "split_many_device",
 ]
 
 
@@ -130,34 +131,55 @@ def split_rows_device(X, fmt: FormatSpec, params: SlicingParams, emu: bool, stre
     """Slice every row of the CUDA float64 matrix view X (rows x kb, unit
     column stride) on the GPU.  Returns (slices, flags); raises the reference's
     exceptions when ``check``."""
+    (ds,), flags = split_many_device([X], fmt, params, emu, stream, check)
+    return ds, flags
+
+
+def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, stream=None,
+                      check: bool = True, flags_out=None):
+    """Slice several matrices with one host synchronisation: all count passes,
+    one read of the slice counts and flags, then all write passes.  Count-pass
+    flags are checked in argument order (the reference slices A before B).
+    Write-pass flags (representability) go to the device word ``flags_out`` if
+    given (checked later by the caller), else they are checked here."""
     torch = _lib.require_cuda()
     if not params.feasible:
         raise SlicingInfeasible(
             f"slice width {params.slice_width} < 0 for m2={params.m2}, m3={params.m3}, k={params.k}")
     code = _fmt_code(fmt)
-    rows, kb = X.shape
-    if X.dtype != torch.float64 or X.stride(1) != 1:
-        raise ValueError("split_rows_device expects a float64 view with unit column stride")
-    ldx = X.stride(0) if rows > 1 else kb
-    dev = X.device
     sp = stream if stream is not None else _lib.stream_ptr(torch)
     eb = _lib.ELEM_BYTES[fmt.name]
-    ld = -(-kb // (16 // eb)) * (16 // eb)
-    row_cnt = torch.zeros(max(rows, 1), dtype=torch.int32, device=dev)
-    small = torch.zeros(2, dtype=torch.int32, device=dev)  # [s_max, flags]
-    _lib.call("oz_split_count", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu),
-              row_cnt.data_ptr(), small.data_ptr(), small.data_ptr() + 4, sp)
-    s_max, flags = (int(v) for v in small.cpu().tolist())
-    flags &= 0xFFFFFFFF
-    if check:
-        _lib.raise_for_flags(flags, "split")
-    planes = torch.empty((s_max, rows, ld * eb), dtype=torch.uint8, device=dev)
-    expo = torch.empty((s_max, rows), dtype=torch.int32, device=dev)
-    if s_max > 0 and rows > 0:
-        small.zero_()
-        _lib.call("oz_split_rows", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu), s_max,
-                  planes.data_ptr(), ld, expo.data_ptr(), row_cnt.data_ptr(), small.data_ptr() + 4, sp)
-    return DeviceSlices(planes, expo, row_cnt[:rows], s_max, rows, kb, ld, fmt), flags
+    metas = []
+    small = torch.zeros(2 * len(Xs) + 1, dtype=torch.int32, device=Xs[0].device)  # [s, flags] per matrix
+    for i, X in enumerate(Xs):
+        rows, kb = X.shape
+        if X.dtype != torch.float64 or (X.stride(1) != 1 and kb > 1):
+            raise ValueError("split expects a float64 view with unit column stride")
+        ldx = X.stride(0) if rows > 1 else kb
+        ld = -(-kb // (16 // eb)) * (16 // eb)
+        row_cnt = torch.zeros(max(rows, 1), dtype=torch.int32, device=X.device)
+        _lib.call("oz_split_count", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu),
+                  row_cnt.data_ptr(), small.data_ptr() + 8 * i, small.data_ptr() + 8 * i + 4, sp)
+        metas.append((X, rows, kb, ldx, ld, row_cnt))
+    host = small.cpu().tolist()  # the one synchronisation
+    out, all_flags = [], 0
+    for i, (X, rows, kb, ldx, ld, row_cnt) in enumerate(metas):
+        s_max, flags = host[2 * i], host[2 * i + 1] & 0xFFFFFFFF
+        all_flags |= flags
+        if check:
+            _lib.raise_for_flags(flags, "split")
+        planes = torch.empty((s_max, rows, ld * eb), dtype=torch.uint8, device=X.device)
+        expo = torch.empty((s_max, rows), dtype=torch.int32, device=X.device)
+        if s_max > 0 and rows > 0:
+            fptr = flags_out.data_ptr() if flags_out is not None else small.data_ptr() + 8 * len(Xs)
+            _lib.call("oz_split_rows", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu), s_max,
+                      planes.data_ptr(), ld, expo.data_ptr(), row_cnt.data_ptr(), fptr, sp)
+        out.append(DeviceSlices(planes, expo, row_cnt[:rows], s_max, rows, kb, ld, fmt))
+    if check and flags_out is None:
+        # representability is checked while encoding (write pass)
+        f = int(small[2 * len(Xs)].item()) & 0xFFFFFFFF
+        _lib.raise_for_flags(f, "split")
+    return out, all_flags
 
 
 def _to_device_f64(M):

@@ -70,11 +70,13 @@ CASES = [
 @pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}x{c[1]}x{c[2]}-{c[4]}-{c[5]}-kb{c[6]}-emu{int(c[7])}"
                                              f"-ms{c[8]}-{c[9][:5]}-cut{c[10]}" for c in CASES])
 @pytest.mark.parametrize("skip", [True, False])
-@pytest.mark.parametrize("cta", ["1", "2"])
-def test_oz_gemm_bitwise(cuda, case, skip, cta, monkeypatch):
+@pytest.mark.parametrize("variant", [("1", "128"), ("2", "128"), ("2", "192")], ids=lambda v: f"cta{v[0]}-n{v[1]}")
+def test_oz_gemm_bitwise(cuda, case, skip, variant, monkeypatch):
     import oracle
 
-    monkeypatch.setenv("OZ_CTA_GROUP", cta)  # read by oz_pair_gemm at each launch
+    # kernel variant, read by oz_pair_gemm at each launch
+    monkeypatch.setenv("OZ_CTA_GROUP", variant[0])
+    monkeypatch.setenv("OZ_TILE_N", variant[1])
 
     oz = _oz()
     m, n, k, phi, t2, t3, kbk, emu, ms, order, cut = case
