@@ -593,23 +593,22 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
       }
 
-      // C = Cb (first block) or C = C + Cb (ozgemm.py:204-207).
-      if (row < P.m) {
-        store_row<kEmu>(P, row, tn * kN + half * 64, cb, 64, flags);
-        if constexpr (kTmHalf > 0) {
+      // C = Cb (first block) or C = C + Cb (ozgemm.py:204-207).  The TMEM reads
+      // are warp-collective (.sync.aligned): issue them outside the row guard.
+      if (row < P.m) store_row<kEmu>(P, row, tn * kN + half * 64, cb, 64, flags);
+      if constexpr (kTmHalf > 0) {
 #pragma unroll
-          for (int ch = 0; ch < kTmHalf / 16; ++ch) {
-            uint32_t w[32];
-            tmem_ld32(cb_tmem + ch * 32, w);
-            tmem_ld_wait();
-            Acc c16[16];
+        for (int ch = 0; ch < kTmHalf / 16; ++ch) {
+          uint32_t w[32];
+          tmem_ld32(cb_tmem + ch * 32, w);
+          tmem_ld_wait();
+          Acc c16[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const uint64_t b = (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
-              if constexpr (kEmu) c16[j] = b; else c16[j] = u2d(b);
-            }
-            store_row<kEmu>(P, row, tn * kN + 128 + half * kTmHalf + ch * 16, c16, 16, flags);
+          for (int j = 0; j < 16; ++j) {
+            const uint64_t b = (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
+            if constexpr (kEmu) c16[j] = b; else c16[j] = u2d(b);
           }
+          if (row < P.m) store_row<kEmu>(P, row, tn * kN + 128 + half * kTmHalf + ch * 16, c16, 16, flags);
         }
       }
     }
