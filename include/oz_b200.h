@@ -49,6 +49,26 @@ enum { OZ_FMT_E4M3 = 0, OZ_FMT_E5M2 = 1, OZ_FMT_FP16 = 2, OZ_FMT_BF16 = 3 };
 #define OZ_FLAG_EMU_RANGE (1u << 5)         /* fp64emu.py:240-241  -> RangeError        */
 #define OZ_FLAG_TERM_RANGE (1u << 6)        /* ozgemm.py:137-139   -> RangeError        */
 #define OZ_FLAG_SUBNORMAL_RESID (1u << 7)   /* fp64emu.py:73-82    -> RangeError        */
+#define OZ_FLAG_PLANE_CAP (1u << 8)         /* oz_split_fused: a row needs > cap planes (re-run two-pass) */
+
+/* One-pass row split (the production path) — replaces slice_matrix(X, "rows",
+ * ...) (slicing.py:190-198) / _slice_rows (slicing.py:128-177): writes each
+ * row's slices as they are produced into coeff[cap][rows][ld_coeff] and
+ * expo[cap][rows], the per-row counts row_cnt[rows] and *s_max = max(*s_max,
+ * max_r row_cnt[r]) (the reference's s, slicing.py:206), plus the validation
+ * and representability flags.  Planes [row_cnt[r], s) of a row are NOT written:
+ * call oz_split_pad once s is known.  A row needing more than `cap` planes sets
+ * OZ_FLAG_PLANE_CAP (outputs then incomplete: use oz_split_count +
+ * oz_split_rows).  kb <= 131072 (clusters of CTAs share rows above 16384). */
+int oz_split_fused(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2, int rho, int emu, int cap,
+                   void* coeff, int64_t ld_coeff, int32_t* expo, int32_t* row_cnt, int32_t* s_max, uint32_t* flags,
+                   void* stream);
+
+/* Zero slices for rows exhausted before the global s (slicing.py:149-152): for
+ * every row r, planes [row_cnt[r], s) of coeff[.][rows][ld_coeff] are zeroed and
+ * their exponents set to 0.  Completes oz_split_fused. */
+int oz_split_pad(void* coeff, int64_t ld_coeff, int64_t rows, int type2, int s, int32_t* expo,
+                 const int32_t* row_cnt, void* stream);
 
 /* Count pass of the row split — replaces the slice-count side of
  * slicing._slice_rows (slicing.py:128-177): per-row slice counts row_cnt[rows],

@@ -27,12 +27,15 @@ FLAG_NOT_REPRESENTABLE = 1 << 4
 FLAG_EMU_RANGE = 1 << 5
 FLAG_TERM_RANGE = 1 << 6
 FLAG_SUBNORMAL_RESID = 1 << 7
+FLAG_PLANE_CAP = 1 << 8  # oz_split_fused only: re-run the exact two-pass split
 
 # Every symbol include/oz_b200.h declares, with its ctypes signature.
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I = ctypes.c_int
 SIGNATURES = {
+    "oz_split_fused": (_I, [_P, _I64, _I64, _I64, _I, _I, _I, _I, _P, _I64, _P, _P, _P, _P, _P]),
+    "oz_split_pad": (_I, [_P, _I64, _I64, _I, _I, _P, _P, _P]),
     "oz_split_count": (_I, [_P, _I64, _I64, _I64, _I, _I, _I, _P, _P, _P, _P]),
     "oz_split_rows": (_I, [_P, _I64, _I64, _I64, _I, _I, _I, _I, _P, _I64, _P, _P, _P, _P]),
     "oz_transpose": (_I, [_P, _I64, _I64, _I64, _P, _I64, _P]),

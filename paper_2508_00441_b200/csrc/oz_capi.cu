@@ -77,33 +77,6 @@ int launch_status() {
   return OZ_OK;
 }
 
-template <bool kWrite>
-int launch_split(const oz::SplitParams& P, int emu, cudaStream_t st) {
-  const int64_t need = (P.ld > P.kb ? P.ld : P.kb);
-  int ept;
-  if (need <= 256 * 4) ept = 4;
-  else if (need <= 256 * 8) ept = 8;
-  else if (need <= 256 * 16) ept = 16;
-  else if (need <= 256 * 32) ept = 32;
-  else if (need <= 256 * 64) ept = 64;
-  else return OZ_EUNSUPPORTED;  // kb > 16384: needs the cluster split (not yet built)
-  const dim3 grid((unsigned)P.rows), block(oz::kSplitThreads);
-#define OZ_SPLIT_CASE(E)                                                              \
-  case E:                                                                             \
-    if (emu) oz::split_rows_kernel<E, kWrite, true><<<grid, block, 0, st>>>(P);       \
-    else oz::split_rows_kernel<E, kWrite, false><<<grid, block, 0, st>>>(P);          \
-    break;
-  switch (ept) {
-    OZ_SPLIT_CASE(4)
-    OZ_SPLIT_CASE(8)
-    OZ_SPLIT_CASE(16)
-    OZ_SPLIT_CASE(32)
-    OZ_SPLIT_CASE(64)
-  }
-#undef OZ_SPLIT_CASE
-  return launch_status();
-}
-
 template <bool kEmu, int kCta, int kEB, int kN>
 int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const oz::PairParams& P, int tiles, cudaStream_t st) {
   const size_t smem = oz::pair_gemm_smem_bytes<kCta, kN>();
@@ -145,9 +118,118 @@ int launch_pair_fmt(const CUtensorMap& ma, const CUtensorMap& mb, const oz::Pair
                            : launch_pair<kEmu, kCta, 2, kN>(ma, mb, P, tiles, st);
 }
 
+// Code tables for the fused split, one per (format, rho), built on first use
+// per device and kept for the process lifetime (a few KB each).
+struct TableKey {
+  int dev, type2, rho;
+};
+std::mutex g_table_mu;
+struct TableEntry {
+  TableKey key;
+  uint32_t* ptr;
+};
+TableEntry g_tables[64];
+int g_ntables = 0;
+
+int code_table(int type2, const LpFormat& f, int rho, cudaStream_t st, const uint32_t** out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_table_mu);
+  for (int i = 0; i < g_ntables; ++i)
+    if (g_tables[i].key.dev == dev && g_tables[i].key.type2 == type2 && g_tables[i].key.rho == rho) {
+      *out = g_tables[i].ptr;
+      return OZ_OK;
+    }
+  if (g_ntables == 64) return OZ_EUNSUPPORTED;
+  const int kmax = 1 << (53 - rho);
+  uint32_t* p = nullptr;
+  if (cudaMalloc(&p, sizeof(uint32_t) * (2 * kmax + 1)) != cudaSuccess) return OZ_ECUDA;
+  oz::build_code_table_kernel<<<(2 * kmax + 1 + 255) / 256, 256, 0, st>>>(p, kmax, rho, f);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return OZ_ECUDA;
+  g_tables[g_ntables++] = {{dev, type2, rho}, p};
+  *out = p;
+  return OZ_OK;
+}
+
+template <int kThreads, int kEPT, int kCL, int kEB, bool kEmu>
+int launch_fused(const oz::FusedSplitParams& P, cudaStream_t st) {
+  auto kern = oz::split_fused_kernel<kThreads, kEPT, kCL, kEB, kEmu>;
+  const size_t smem = sizeof(uint32_t) * (2 * P.kmax + 1);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(P.rows * kCL));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = kCL > 1 ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, P);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "oz_b200: split launch failed: %s\n", cudaGetErrorString(e));
+    return OZ_ECUDA;
+  }
+  return launch_status();
+}
+
+template <int kEB, bool kEmu>
+int launch_fused_cfg(const oz::FusedSplitParams& P, cudaStream_t st) {
+  const int64_t need = P.ld > P.kb ? P.ld : P.kb;
+  if (need <= 1024) return launch_fused<64, 16, 1, kEB, kEmu>(P, st);
+  if (need <= 2048) return launch_fused<128, 16, 1, kEB, kEmu>(P, st);
+  if (need <= 4096) return launch_fused<256, 16, 1, kEB, kEmu>(P, st);
+  if (need <= 8192) return launch_fused<256, 32, 1, kEB, kEmu>(P, st);
+  if (need <= 16384) return launch_fused<512, 32, 1, kEB, kEmu>(P, st);
+  if (need <= 32768) return launch_fused<256, 32, 4, kEB, kEmu>(P, st);
+  if (need <= 65536) return launch_fused<256, 32, 8, kEB, kEmu>(P, st);
+  if (need <= 131072) return launch_fused<512, 32, 8, kEB, kEmu>(P, st);
+  return OZ_EUNSUPPORTED;
+}
+
 }  // namespace
 
 extern "C" {
+
+int oz_split_fused(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2, int rho, int emu, int cap,
+                   void* coeff, int64_t ld_coeff, int32_t* expo, int32_t* row_cnt, int32_t* s_max, uint32_t* flags,
+                   void* stream) {
+  LpFormat f;
+  uint32_t idf;
+  if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
+  if (rows < 0 || kb < 1 || ldx < kb || ld_coeff < kb || cap < 0 || !X || !row_cnt || !s_max || !flags)
+    return OZ_EINVAL;
+  if ((ld_coeff * f.bytes) % 16) return OZ_EINVAL;
+  if (rho < 42 || rho > 53) return OZ_EUNSUPPORTED;  // |k| <= 2^(53-rho) table; rho >= xi >= 42 for our formats
+  if (rows == 0) return OZ_OK;
+  if (cap > 0 && (!coeff || !expo)) return OZ_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  oz::FusedSplitParams P{};
+  P.X = X; P.rows = rows; P.kb = kb; P.ldx = ldx; P.rho = rho; P.cap = cap;
+  P.coeff = static_cast<uint8_t*>(coeff); P.ld = ld_coeff; P.expo = expo; P.row_cnt = row_cnt;
+  P.s_max = s_max; P.flags = flags; P.kmax = 1 << (53 - rho);
+  int rc = code_table(type2, f, rho, st, &P.table);
+  if (rc) return rc;
+  if (f.bytes == 1) return emu ? launch_fused_cfg<1, true>(P, st) : launch_fused_cfg<1, false>(P, st);
+  return emu ? launch_fused_cfg<2, true>(P, st) : launch_fused_cfg<2, false>(P, st);
+}
+
+int oz_split_pad(void* coeff, int64_t ld_coeff, int64_t rows, int type2, int s, int32_t* expo,
+                 const int32_t* row_cnt, void* stream) {
+  LpFormat f;
+  uint32_t idf;
+  if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
+  if (rows < 0 || s < 0 || (ld_coeff * f.bytes) % 16) return OZ_EINVAL;
+  if (rows == 0 || s == 0) return OZ_OK;
+  if (!coeff || !expo || !row_cnt) return OZ_EINVAL;
+  const unsigned blocks = (unsigned)((rows + 7) / 8);
+  oz::pad_planes_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<uint8_t*>(coeff), ld_coeff * f.bytes,
+                                                                   rows, s, expo, row_cnt);
+  return launch_status();
+}
 
 const char* oz_version(void) { return "oz_b200 0.1 (sm_100a tcgen05; reference ozdgemm 1.0.0 semantics)"; }
 
@@ -165,30 +247,33 @@ const char* oz_strerror(int status) {
 
 int oz_split_count(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2, int rho, int emu,
                    int32_t* row_cnt, int32_t* s_max, uint32_t* flags, void* stream) {
-  oz::SplitParams P{};
+  // Count-only mode of the fused split (no coefficient buffer).
+  LpFormat f;
   uint32_t idf;
-  if (!fmt_info(type2, P.fmt, idf)) return OZ_EUNSUPPORTED;
+  if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
   if (rows < 0 || kb < 1 || ldx < kb || !X || !row_cnt || !s_max || !flags) return OZ_EINVAL;
-  if (rows == 0) return OZ_OK;
-  P.X = X; P.rows = rows; P.kb = kb; P.ldx = ldx; P.rho = rho;
-  P.planes = 0; P.coeff = nullptr; P.ld = kb; P.expo = nullptr;
-  P.row_cnt = row_cnt; P.s_max = s_max; P.flags = flags;
-  return launch_split<false>(P, emu, (cudaStream_t)stream);
+  const int64_t ld = (kb + 15) / 16 * 16;
+  return oz_split_fused(X, rows, kb, ldx, type2, rho, emu, 0, nullptr, ld, nullptr, row_cnt, s_max, flags, stream);
 }
 
 int oz_split_rows(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2, int rho, int emu, int planes,
                   void* coeff, int64_t ld_coeff, int32_t* expo, int32_t* row_cnt, uint32_t* flags, void* stream) {
-  oz::SplitParams P{};
+  // Exactly `planes` planes: fused split with cap = planes, then zero padding.
+  LpFormat f;
   uint32_t idf;
-  if (!fmt_info(type2, P.fmt, idf)) return OZ_EUNSUPPORTED;
+  if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
   if (rows < 0 || kb < 1 || ldx < kb || ld_coeff < kb || planes < 0 || !X || !row_cnt || !flags) return OZ_EINVAL;
-  if ((ld_coeff * P.fmt.bytes) % 16) return OZ_EINVAL;
+  if ((ld_coeff * f.bytes) % 16) return OZ_EINVAL;
   if (rows == 0 || planes == 0) return OZ_OK;
   if (!coeff || !expo) return OZ_EINVAL;
-  P.X = X; P.rows = rows; P.kb = kb; P.ldx = ldx; P.rho = rho;
-  P.planes = planes; P.coeff = static_cast<uint8_t*>(coeff); P.ld = ld_coeff; P.expo = expo;
-  P.row_cnt = row_cnt; P.s_max = nullptr; P.flags = flags;
-  return launch_split<true>(P, emu, (cudaStream_t)stream);
+  int32_t* s_scratch = nullptr;
+  if (cudaMallocAsync(&s_scratch, sizeof(int32_t), (cudaStream_t)stream) != cudaSuccess) return OZ_ECUDA;
+  cudaMemsetAsync(s_scratch, 0, sizeof(int32_t), (cudaStream_t)stream);
+  int rc = oz_split_fused(X, rows, kb, ldx, type2, rho, emu, planes, coeff, ld_coeff, expo, row_cnt, s_scratch,
+                          flags, stream);
+  cudaFreeAsync(s_scratch, (cudaStream_t)stream);
+  if (rc) return rc;
+  return oz_split_pad(coeff, ld_coeff, rows, type2, planes, expo, row_cnt, stream);
 }
 
 int oz_transpose(const double* src, int64_t rows, int64_t cols, int64_t ld_src, double* dst, int64_t ld_dst,

@@ -1,28 +1,23 @@
 // oz_split.cu — K1/K2: error-free splitting of FP64 rows into power-of-two-scaled
 // low-precision slices (restates slicing._slice_rows, slicing.py:128-177).
 //
-// One CTA owns one row of length kb; the row lives in registers (kEPT doubles
-// per thread, 256 threads, kb <= 256*kEPT).  Every iteration of the reference
-// loop (slicing.py:144-176) becomes:
-//   * CTA max of |x| as an integer max over the sign-cleared bit patterns
-//     (fp64emu.max_abs, fp64emu.py:315-319) — warp shuffles + one smem hop;
-//   * c = ceil(log2 max) from the bit pattern (fp64emu.py:280-284);
+// One CTA (or a cluster of CTAs for kb > 16384) owns one row; the row lives in
+// registers.  Every iteration of the reference loop (slicing.py:144-176) becomes:
+//   * the row max of ceil_log2|x| (fp64emu.max_abs + ceil_log2_abs,
+//     fp64emu.py:280-284, 315-319) as one u32 max per element + redux.sync;
 //   * sigma = 1.5 * 2^(c+rho-1) assembled as bits (slicing.py:153-160);
-//   * v = (x + sigma) - sigma ; x = x - v ; coeff = v * 2^-c (slicing.py:162-168)
-//     with __dadd_rn/__dsub_rn (HW) or the integer emu_add (EMU);
-//   * coeff encoded straight from its FP64 bit pattern into E4M3/E5M2/FP16/BF16
-//     bits (integer only, exact; non-representable sets a flag — slicing.py:169-172).
-// The split runs twice: a count pass (per-row slice count, global s via
-// atomicMax, validation flags) and a write pass that emits exactly s planes
-// (rows exhausted early get zero slices with exponent 0, slicing.py:149-152).
+//   * v = (x + sigma) - sigma ; x = x - v (slicing.py:162-168) with
+//     __dadd_rn/__dsub_rn (HW) or the integer emu_add (EMU);
+//   * coeff = v * 2^-c = k * 2^(rho-53) encoded by table lookup on k
+//     (slicing.py:168-172; table built with the exact generic encoder).
+// One pass writes the slices as they are produced (see split_fused_kernel);
+// a count-only mode of the same kernel serves the exact two-pass fallback.
 // Output layout: coeff[p][row][ld] (K-major, ld a multiple of 16 bytes),
-// expo[p][row] int32.  Columns of B are sliced by transposing B first.
+// expo[p][row] int32.  Columns of B are sliced by transposing B first (K2).
 #include "oz_common.cuh"
 
 namespace oz {
 
-constexpr int kSplitThreads = 256;
-constexpr int kV = 4;  // consecutive elements per thread chunk
 constexpr int kHardSlices = 2100;  // slicing.py:38
 
 struct LpFormat {
@@ -30,20 +25,6 @@ struct LpFormat {
   int max_field;    // largest exponent field holding finite values
   int nan_top;      // 1: the all-ones mantissa in max_field is NaN (E4M3)
   int bytes;
-};
-
-struct SplitParams {
-  const double* X;
-  int64_t rows, kb, ldx;
-  int rho;
-  LpFormat fmt;
-  int planes;        // write pass: number of planes to emit (= global s)
-  uint8_t* coeff;    // [planes][rows][ld]
-  int64_t ld;        // elements
-  int32_t* expo;     // [planes][rows]
-  int32_t* row_cnt;  // [rows]
-  int32_t* s_max;    // count pass
-  uint32_t* flags;
 };
 
 // FP64 bit pattern of a slice value v (a multiple of 2^(c+rho-53), |v| <= 2^c)
@@ -74,159 +55,246 @@ OZ_DEVICE uint32_t encode_coeff(uint64_t vb, int c, const LpFormat& f, uint32_t&
   return sign | code;
 }
 
-OZ_DEVICE uint64_t warp_max_u64(uint64_t v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint64_t w = __shfl_xor_sync(0xFFFFFFFFu, v, o);
-    v = w > v ? w : v;
-  }
-  return v;
+// ─────────────────────── K1 fused: one pass, table encode ───────────────────────
+// The production split:
+//   * ONE pass: slices are written as they are produced into a buffer of `cap`
+//     planes; the global s is an atomicMax of the row counts, and rows that end
+//     early are zero-padded afterwards by pad_planes_kernel (only the missing
+//     planes are written).  A row needing more than `cap` planes raises
+//     FLAG_PLANE_CAP and the host re-runs the exact two-pass split.
+//   * The slice integer comes straight out of the shifted sum: xs = x + sigma
+//     stays in sigma's binade (|x| <= 2^c << sigma = 1.5*2^(c+rho-1)) whose ulp is
+//     q = 2^(c+rho-53), so bits(xs) = bits(sigma) + k with k*q = RN_q(x), and
+//     sigma's low word is 0: k = (int)lo32(xs).  coeff = k*2^(rho-53), so the
+//     type2 code is a lookup table over |k| <= 2^(53-rho) built once with the
+//     generic encoder (it carries the representability bit, slicing.py:169-172).
+//   * The next slice exponent needs only ceil_log2(max|x|) = max over elements
+//     of ceil_log2|x|; the 32-bit key (hi32(x) << 1) | (lo32(x) != 0) orders
+//     elements by exactly that, so each iteration is one u32 max (redux.sync).
+//   * Residuals are multiples of ulp(x_original): when every input of a thread
+//     has exponent >= -969 no residual can be subnormal, and the per-element
+//     subnormal-residual check (max_abs, fp64emu.py:73-82) is skipped.
+//   * kCL > 1: a cluster of kCL CTAs shares one row (kb up to kCL*kThreads*kEPT);
+//     the per-iteration max goes through DSMEM and a cluster barrier.
+// Each thread owns runs of kV = 16/kEB consecutive elements, so every plane
+// store is one 16-byte vector.
+constexpr uint32_t FLAG_PLANE_CAP_INTERNAL = 1u << 8;  // host falls back to the two-pass split
+
+struct FusedSplitParams {
+  const double* X;
+  int64_t rows, kb, ldx;
+  int rho;
+  int cap;                 // planes allocated in coeff / expo
+  uint8_t* coeff;          // [cap][rows][ld]
+  int64_t ld;              // elements
+  int32_t* expo;           // [cap][rows]
+  int32_t* row_cnt;        // [rows]
+  int32_t* s_max;          // atomicMax
+  uint32_t* flags;
+  const uint32_t* table;   // [2K+1] code | (not_representable << 16), index k + K
+  int kmax;                // K = 2^(53-rho)
+};
+
+// table[k + K] = code of k * 2^(rho-53) (| 1<<16 if not representable).
+__global__ void build_code_table_kernel(uint32_t* table, int kmax, int rho, LpFormat f) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > 2 * kmax) return;
+  const int k = i - kmax;
+  uint32_t fl = 0;
+  const double v = (double)k * ldexp(1.0, rho - 53);
+  const uint32_t code = encode_coeff(d2u(v), 0, f, fl);
+  table[i] = code | (fl ? (1u << 16) : 0u);
 }
 
-template <int kEPT, bool kWrite, bool kEmu>
-__global__ void __launch_bounds__(kSplitThreads) split_rows_kernel(const SplitParams P) {
+OZ_DEVICE uint32_t elem_key(uint64_t x) {
+  const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+  return (hi << 1) | (lo != 0u ? 1u : 0u);
+}
+
+OZ_DEVICE void st_cluster_u32(uint32_t* local_addr, uint32_t rank, uint32_t v) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local_addr)), "r"(rank));
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(remote), "r"(v) : "memory");
+}
+
+OZ_DEVICE void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+OZ_DEVICE uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+template <int kThreads, int kEPT, int kCL, int kEB, bool kEmu>
+__global__ void __launch_bounds__(kThreads) split_fused_kernel(const FusedSplitParams P) {
+  constexpr int kV = 16 / kEB;          // elements per 16-byte plane store
   constexpr int kChunks = kEPT / kV;
-  __shared__ uint64_t red[2][kSplitThreads / 32];
-  const int64_t row = blockIdx.x;
+  constexpr int kWarps = kThreads / 32;
+  static_assert(kEPT % kV == 0, "EPT must be a multiple of the store vector");
+  __shared__ uint32_t red_w[2][kWarps];
+  __shared__ uint32_t red_c[2][kCL];
+  extern __shared__ uint32_t tbl[];      // 2K+1 entries
+
+  const uint32_t rank = kCL > 1 ? cluster_ctarank() : 0u;
+  const int64_t row = blockIdx.x / kCL;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int64_t base = (int64_t)rank * kThreads * kEPT;  // first element of this CTA's part
   const double* xr = P.X + row * P.ldx;
   const bool aligned = ((reinterpret_cast<uintptr_t>(xr) & 15) == 0);
-  uint32_t flags = 0;
+  const int K = P.kmax;
+  for (int i = t; i <= 2 * K; i += kThreads) tbl[i] = __ldg(P.table + i);
+  uint32_t flags = 0, bad = 0;
 
-  uint64_t x[kEPT];  // residual as bit patterns
+  uint64_t x[kEPT];
+  const uint64_t* xw = reinterpret_cast<const uint64_t*>(xr);
 #pragma unroll
   for (int c = 0; c < kChunks; ++c) {
-    const int64_t e0 = ((int64_t)c * kSplitThreads + t) * kV;
-    // Loaded as raw 64-bit words: no double-typed value in the emulated kernels.
-    const uint64_t* xw = reinterpret_cast<const uint64_t*>(xr);
+    const int64_t e0 = base + ((int64_t)c * kThreads + t) * kV;
     if (aligned && e0 + kV <= P.kb) {
-      const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(xw + e0);
-      const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(xw + e0 + 2);
-      x[c * kV + 0] = a.x;
-      x[c * kV + 1] = a.y;
-      x[c * kV + 2] = b.x;
-      x[c * kV + 3] = b.y;
+#pragma unroll
+      for (int u = 0; u < kV; u += 2) {
+        const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(xw + e0 + u);
+        x[c * kV + u] = a.x;
+        x[c * kV + u + 1] = a.y;
+      }
     } else {
 #pragma unroll
       for (int u = 0; u < kV; ++u) x[c * kV + u] = (e0 + u < P.kb) ? xw[e0 + u] : 0ull;
     }
   }
-  // _validate_input (slicing.py:119-125).
+  // _validate_input (slicing.py:119-125) + the first max key.
+  bool tiny = false;
+  uint32_t key = 0;
 #pragma unroll
   for (int i = 0; i < kEPT; ++i) {
     const uint32_t ef = (uint32_t)((x[i] >> 52) & 0x7FF);
     if (ef == 2047) flags |= FLAG_NONFINITE_INPUT;
     else if (ef == 0 && (x[i] << 1) != 0) flags |= FLAG_SUBNORMAL_INPUT;
+    if (ef < 1023 - 969 && (x[i] << 1) != 0) tiny = true;
   }
   if (flags & FLAG_NONFINITE_INPUT) {
 #pragma unroll
     for (int i = 0; i < kEPT; ++i) x[i] = 0;  // keep the loop finite; host raises
   }
+#pragma unroll
+  for (int i = 0; i < kEPT; ++i) key = max(key, elem_key(x[i]));
+  if constexpr (kCL > 1) cluster_barrier();  // peers running before any DSMEM store
+  else __syncthreads();                      // table visible
 
-  const int64_t plane_stride = P.rows * P.ld * P.fmt.bytes;  // bytes
+  const int64_t plane_stride = P.rows * P.ld * kEB;  // bytes
+  uint8_t* const row_plane0 = P.coeff + row * P.ld * kEB;
+  const bool write = P.coeff != nullptr;  // count-only mode otherwise (no planes, no exponents)
   int cnt = 0;
   for (int it = 0;; ++it) {
-    uint64_t m = 0;
-#pragma unroll
-    for (int i = 0; i < kEPT; ++i) {
-      const uint64_t a = x[i] & ~kSign;
-      m = a > m ? a : m;
-    }
-    m = warp_max_u64(m);
-    if (lane == 0) red[it & 1][wid] = m;
+    // Row max of the key: warp redux -> smem -> (cluster DSMEM).
+    uint32_t m = __reduce_max_sync(0xFFFFFFFFu, key);
+    if (lane == 0) red_w[it & 1][wid] = m;
     __syncthreads();
     m = 0;
 #pragma unroll
-    for (int w = 0; w < kSplitThreads / 32; ++w) m = red[it & 1][w] > m ? red[it & 1][w] : m;
+    for (int w = 0; w < kWarps; ++w) m = max(m, red_w[it & 1][w]);
+    if constexpr (kCL > 1) {
+      if (t < kCL) st_cluster_u32(&red_c[it & 1][rank], (uint32_t)t, m);
+      cluster_barrier();
+      m = 0;
+#pragma unroll
+      for (int r = 0; r < kCL; ++r) m = max(m, red_c[it & 1][r]);
+    }
     if (m == 0) break;
-    if (it >= kHardSlices || (kWrite && it >= P.planes)) {
+    if (it >= kHardSlices) {
       flags |= FLAG_SLICE_CAP;
       break;
     }
-    // c = ceil(log2 max|x|) from the bit pattern.
-    const int e = (int)(m >> 52) - 1023;
-    const int c = (m & kFracMask) == 0 ? e : e + 1;
+    if (write && it >= P.cap) {
+      flags |= FLAG_PLANE_CAP_INTERNAL;
+      break;
+    }
+    // c = ceil(log2 max|x|): exponent field = key >> 21, fraction non-zero = low 21 key bits.
+    const int e = (int)(m >> 21) - 1023;
+    const int c = (m & 0x1FFFFFu) != 0 ? e + 1 : e;
     const int sig_exp = c + P.rho - 1 + 1023;
     if (sig_exp < 1 || sig_exp > 2046) {
       flags |= FLAG_SIGMA_RANGE;
       break;
     }
     const uint64_t sigma = ((uint64_t)sig_exp << 52) | (1ull << 51);
-    uint32_t codes[kEPT];
+    uint8_t* plane = row_plane0 + (int64_t)it * plane_stride;
+    key = 0;
 #pragma unroll
-    for (int i = 0; i < kEPT; ++i) {
-      uint64_t v;
-      if constexpr (kEmu) {
-        v = emu_add(emu_add(x[i], sigma, flags), sigma ^ kSign, flags);
-        x[i] = emu_add(x[i], v ^ kSign, flags);
-      } else {
-        const double xs = __dadd_rn(u2d(x[i]), u2d(sigma));
-        v = d2u(__dsub_rn(xs, u2d(sigma)));
-        x[i] = d2u(__dsub_rn(u2d(x[i]), u2d(v)));
-      }
-      const uint32_t ef = (uint32_t)((x[i] >> 52) & 0x7FF);
-      if (ef == 0 && (x[i] << 1) != 0) flags |= FLAG_SUBNORMAL_RESID;
-      if constexpr (kWrite) codes[i] = encode_coeff(v, c, P.fmt, flags);  // count pass: no codes
-      else (void)codes;
-    }
-    if constexpr (kWrite) {
-      uint8_t* plane = P.coeff + (int64_t)it * plane_stride + row * P.ld * P.fmt.bytes;
+    for (int ch = 0; ch < kChunks; ++ch) {
+      uint32_t codes[kV];
 #pragma unroll
-      for (int ch = 0; ch < kChunks; ++ch) {
-        const int64_t e0 = ((int64_t)ch * kSplitThreads + t) * kV;
-        if (e0 < P.ld) {
-          if (P.fmt.bytes == 1) {
-            const uint32_t w = codes[ch * kV] | (codes[ch * kV + 1] << 8) | (codes[ch * kV + 2] << 16) |
-                               (codes[ch * kV + 3] << 24);
-            *reinterpret_cast<uint32_t*>(plane + e0) = w;
-          } else {
-            uint2 w;
-            w.x = codes[ch * kV] | (codes[ch * kV + 1] << 16);
-            w.y = codes[ch * kV + 2] | (codes[ch * kV + 3] << 16);
-            *reinterpret_cast<uint2*>(plane + e0 * 2) = w;
-          }
+      for (int u = 0; u < kV; ++u) {
+        const int i = ch * kV + u;
+        uint64_t xs, v;
+        if constexpr (kEmu) {
+          xs = emu_add(x[i], sigma, flags);
+          v = emu_add(xs, sigma ^ kSign, flags);
+          x[i] = emu_add(x[i], v ^ kSign, flags);
+        } else {
+          const double xsd = __dadd_rn(u2d(x[i]), u2d(sigma));
+          xs = d2u(xsd);
+          v = d2u(__dsub_rn(xsd, u2d(sigma)));
+          x[i] = d2u(__dsub_rn(u2d(x[i]), u2d(v)));
+        }
+        if (write) {
+          int k = (int)(uint32_t)xs;  // slice integer: coeff = k * 2^(rho-53)
+          if constexpr (kEmu) k = min(max(k, -K), K);  // only reachable after a flagged range error
+          const uint32_t ent = tbl[k + K];
+          bad |= ent;
+          codes[u] = ent;
+        }
+        key = max(key, elem_key(x[i]));
+        if (tiny) {
+          const uint32_t ef = (uint32_t)((x[i] >> 52) & 0x7FF);
+          if (ef == 0 && (x[i] << 1) != 0) flags |= FLAG_SUBNORMAL_RESID;
         }
       }
-      if (t == 0) P.expo[(int64_t)it * P.rows + row] = c;
+      const int64_t e0 = base + ((int64_t)ch * kThreads + t) * kV;
+      if (write && e0 < P.ld) {
+        uint4 w;
+        if constexpr (kEB == 1) {
+          w.x = __byte_perm(__byte_perm(codes[0], codes[1], 0x0040), __byte_perm(codes[2], codes[3], 0x0040), 0x5410);
+          w.y = __byte_perm(__byte_perm(codes[4], codes[5], 0x0040), __byte_perm(codes[6], codes[7], 0x0040), 0x5410);
+          w.z = __byte_perm(__byte_perm(codes[8], codes[9], 0x0040), __byte_perm(codes[10], codes[11], 0x0040), 0x5410);
+          w.w = __byte_perm(__byte_perm(codes[12], codes[13], 0x0040), __byte_perm(codes[14], codes[15], 0x0040), 0x5410);
+        } else {
+          w.x = __byte_perm(codes[0], codes[1], 0x5410);
+          w.y = __byte_perm(codes[2], codes[3], 0x5410);
+          w.z = __byte_perm(codes[4], codes[5], 0x5410);
+          w.w = __byte_perm(codes[6], codes[7], 0x5410);
+        }
+        *reinterpret_cast<uint4*>(plane + e0 * kEB) = w;
+      }
     }
+    if (write && t == 0 && rank == 0) P.expo[(int64_t)it * P.rows + row] = c;
     ++cnt;
   }
-  if constexpr (kWrite) {
-    // Zero slices for a row exhausted before the global s (slicing.py:149-152).
-    for (int p = cnt; p < P.planes; ++p) {
-      uint8_t* plane = P.coeff + (int64_t)p * plane_stride + row * P.ld * P.fmt.bytes;
-#pragma unroll
-      for (int ch = 0; ch < kChunks; ++ch) {
-        const int64_t e0 = ((int64_t)ch * kSplitThreads + t) * kV;
-        if (e0 < P.ld) {
-          if (P.fmt.bytes == 1)
-            *reinterpret_cast<uint32_t*>(plane + e0) = 0u;
-          else
-            *reinterpret_cast<uint2*>(plane + e0 * 2) = make_uint2(0u, 0u);
-        }
-      }
-      if (t == 0) P.expo[(int64_t)p * P.rows + row] = 0;
-    }
-  }
-  if (t == 0) {
+  if (bad & (1u << 16)) flags |= FLAG_NOT_REPRESENTABLE;
+  if (t == 0 && rank == 0) {
     P.row_cnt[row] = cnt;
-    if constexpr (!kWrite) atomicMax(P.s_max, cnt);
+    atomicMax(P.s_max, cnt);
   }
-  // Combine flags across the CTA with one atomic per warp that saw something.
   flags = __reduce_or_sync(0xFFFFFFFFu, flags);
   if (lane == 0 && flags) atomicOr(P.flags, flags);
 }
 
-#define OZ_SPLIT_INST(EPT)                                                       \
-  template __global__ void split_rows_kernel<EPT, false, false>(const SplitParams); \
-  template __global__ void split_rows_kernel<EPT, true, false>(const SplitParams);  \
-  template __global__ void split_rows_kernel<EPT, false, true>(const SplitParams);  \
-  template __global__ void split_rows_kernel<EPT, true, true>(const SplitParams);
-OZ_SPLIT_INST(4)
-OZ_SPLIT_INST(8)
-OZ_SPLIT_INST(16)
-OZ_SPLIT_INST(32)
-OZ_SPLIT_INST(64)
+// Zero slices for rows exhausted before the global s (slicing.py:149-152):
+// planes [row_cnt[row], s) of each row and their exponents.  One warp per row.
+__global__ void pad_planes_kernel(uint8_t* __restrict__ coeff, int64_t row_bytes, int64_t rows, int s,
+                                  int32_t* __restrict__ expo, const int32_t* __restrict__ row_cnt) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (row >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const int cnt = row_cnt[row];
+  for (int p = cnt; p < s; ++p) {
+    uint4* dst = reinterpret_cast<uint4*>(coeff + ((int64_t)p * rows + row) * row_bytes);
+    for (int64_t i = lane; i < row_bytes / 16; i += 32) dst[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (lane == 0) expo[(int64_t)p * rows + row] = 0;
+  }
+}
 
 // dst[j][i] = src[i][j]  (rows x cols -> cols x rows), 32x32 smem tiles.
 __global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict__ src, int64_t rows, int64_t cols,

@@ -4,10 +4,12 @@ Host-side planning mirrors ``ozdgemm.slicing`` (slicing.py:45-97): the same
 ``SlicingParams`` / ``compute_params`` / ``predict_*`` contract.  The slicing
 itself (slicing.py:128-206) runs on the GPU in ``oz_split.cu``:
 
-  1. count pass  (``oz_split_count``): per-row slice counts, the global slice
-     count s, validation flags;
-  2. write pass  (``oz_split_rows``): exactly s planes of FP8/FP16 codes,
-     K-major ``[s][rows][ld]``, plus int32 exponents ``[s][rows]``.
+  1. one fused pass (``oz_split_fused``): FP8/FP16 code planes, K-major
+     ``[s][rows][ld]``, int32 exponents ``[s][rows]``, per-row slice counts,
+     the global slice count s and the validation flags;
+  2. ``oz_split_pad`` zero-fills the planes of rows that ended before s.
+  (Exact two-pass fallback, ``oz_split_count`` + ``oz_split_rows``, when a
+  row needs more planes than were allocated.)
 
 Columns of B are sliced by transposing B on the device first (the reference
 does the same transpose on the host, slicing.py:199-203).  ``slice_matrix``
@@ -19,6 +21,7 @@ device planes (``DeviceSlices``) and never decodes them.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -135,13 +138,28 @@ def split_rows_device(X, fmt: FormatSpec, params: SlicingParams, emu: bool, stre
     return ds, flags
 
 
+PLANE_CAP = int(os.environ.get("OZ_PLANE_CAP", "32"))
+PLANE_BUDGET_BYTES = 24 << 30  # per operand; larger operands start with fewer planes
+
+
+def _plane_cap(rows: int, row_bytes: int, predicted: int) -> int:
+    per_plane = max(rows * row_bytes, 1)
+    cap = min(PLANE_CAP, max(PLANE_BUDGET_BYTES // per_plane, 1))
+    return max(cap, min(predicted + 4, PLANE_CAP), 1)
+
+
 def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, stream=None,
                       check: bool = True, flags_out=None):
-    """Slice several matrices with one host synchronisation: all count passes,
-    one read of the slice counts and flags, then all write passes.  Count-pass
-    flags are checked in argument order (the reference slices A before B).
-    Write-pass flags (representability) go to the device word ``flags_out`` if
-    given (checked later by the caller), else they are checked here."""
+    """Slice several matrices with one host synchronisation.
+
+    Fast path: one fused pass per matrix (``oz_split_fused``) writes the slices
+    into a buffer of ``cap`` planes while counting; after the single sync that
+    reads every s and flag word, ``oz_split_pad`` zero-fills the planes of rows
+    that ended early.  A matrix with a row needing more than ``cap`` planes is
+    re-sliced exactly with the two-pass path (count, then write s planes).
+    Flags are checked in argument order (the reference slices A before B).
+    Representability flags go to the device word ``flags_out`` if given
+    (checked later by the caller), else they are checked here."""
     torch = _lib.require_cuda()
     if not params.feasible:
         raise SlicingInfeasible(
@@ -149,36 +167,63 @@ def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, str
     code = _fmt_code(fmt)
     sp = stream if stream is not None else _lib.stream_ptr(torch)
     eb = _lib.ELEM_BYTES[fmt.name]
+    predicted = predict_slice_count(params) or 1
     metas = []
-    small = torch.zeros(2 * len(Xs) + 1, dtype=torch.int32, device=Xs[0].device)  # [s, flags] per matrix
+    small = torch.zeros(2 * len(Xs), dtype=torch.int32, device=Xs[0].device)  # [s, flags] per matrix
     for i, X in enumerate(Xs):
         rows, kb = X.shape
         if X.dtype != torch.float64 or (X.stride(1) != 1 and kb > 1):
             raise ValueError("split expects a float64 view with unit column stride")
         ldx = X.stride(0) if rows > 1 else kb
         ld = -(-kb // (16 // eb)) * (16 // eb)
+        cap = _plane_cap(rows, ld * eb, predicted)
         row_cnt = torch.zeros(max(rows, 1), dtype=torch.int32, device=X.device)
-        _lib.call("oz_split_count", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu),
-                  row_cnt.data_ptr(), small.data_ptr() + 8 * i, small.data_ptr() + 8 * i + 4, sp)
-        metas.append((X, rows, kb, ldx, ld, row_cnt))
+        planes = torch.empty((cap, rows, ld * eb), dtype=torch.uint8, device=X.device)
+        expo = torch.empty((cap, rows), dtype=torch.int32, device=X.device)
+        if rows > 0:
+            _lib.call("oz_split_fused", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu), cap,
+                      planes.data_ptr(), ld, expo.data_ptr(), row_cnt.data_ptr(),
+                      small.data_ptr() + 8 * i, small.data_ptr() + 8 * i + 4, sp)
+        metas.append((X, rows, kb, ldx, ld, row_cnt, planes, expo))
     host = small.cpu().tolist()  # the one synchronisation
     out, all_flags = [], 0
-    for i, (X, rows, kb, ldx, ld, row_cnt) in enumerate(metas):
+    for i, (X, rows, kb, ldx, ld, row_cnt, planes, expo) in enumerate(metas):
         s_max, flags = host[2 * i], host[2 * i + 1] & 0xFFFFFFFF
+        if flags & _lib.FLAG_PLANE_CAP:
+            # Some row needs more planes than allocated: exact two-pass split.
+            del planes, expo
+            cnt = torch.zeros(2, dtype=torch.int32, device=X.device)
+            _lib.call("oz_split_count", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu),
+                      row_cnt.data_ptr(), cnt.data_ptr(), cnt.data_ptr() + 4, sp)
+            s_max, flags = (int(v) for v in cnt.cpu().tolist())
+            flags &= 0xFFFFFFFF
+            if check:
+                _lib.raise_for_flags(flags, "split")
+            planes = torch.empty((s_max, rows, ld * eb), dtype=torch.uint8, device=X.device)
+            expo = torch.empty((s_max, rows), dtype=torch.int32, device=X.device)
+            if s_max > 0:
+                fw = torch.zeros(1, dtype=torch.int32, device=X.device)
+                _lib.call("oz_split_rows", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu), s_max,
+                          planes.data_ptr(), ld, expo.data_ptr(), row_cnt.data_ptr(),
+                          (flags_out if flags_out is not None else fw).data_ptr(), sp)
+                if check and flags_out is None:
+                    _lib.raise_for_flags(int(fw.item()) & 0xFFFFFFFF, "split")
+        else:
+            rep = flags & _lib.FLAG_NOT_REPRESENTABLE
+            flags &= ~_lib.FLAG_NOT_REPRESENTABLE
+            if check:
+                _lib.raise_for_flags(flags, "split")
+            if rep:
+                if flags_out is not None:
+                    flags_out.bitwise_or_(rep)
+                elif check:
+                    _lib.raise_for_flags(rep, "split")
+            planes, expo = planes[:s_max], expo[:s_max]
+            if s_max > 0 and rows > 0:
+                _lib.call("oz_split_pad", planes.data_ptr(), ld, rows, code, s_max, expo.data_ptr(),
+                          row_cnt.data_ptr(), sp)
         all_flags |= flags
-        if check:
-            _lib.raise_for_flags(flags, "split")
-        planes = torch.empty((s_max, rows, ld * eb), dtype=torch.uint8, device=X.device)
-        expo = torch.empty((s_max, rows), dtype=torch.int32, device=X.device)
-        if s_max > 0 and rows > 0:
-            fptr = flags_out.data_ptr() if flags_out is not None else small.data_ptr() + 8 * len(Xs)
-            _lib.call("oz_split_rows", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu), s_max,
-                      planes.data_ptr(), ld, expo.data_ptr(), row_cnt.data_ptr(), fptr, sp)
         out.append(DeviceSlices(planes, expo, row_cnt[:rows], s_max, rows, kb, ld, fmt))
-    if check and flags_out is None:
-        # representability is checked while encoding (write pass)
-        f = int(small[2 * len(Xs)].item()) & 0xFFFFFFFF
-        _lib.raise_for_flags(f, "split")
     return out, all_flags
 
 

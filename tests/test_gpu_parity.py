@@ -119,3 +119,57 @@ def test_lp_gemm_exact_on_slices(cuda):
         for q in (0, sb.s - 1):
             G = oz.lp_gemm(oz.LpMatrix(sa.coeff[p], f), oz.LpMatrix(sb.coeff[q], f), oz.get_format("fp32"))
             assert np.array_equal(G, sa.coeff[p] @ sb.coeff[q])
+
+
+@pytest.mark.parametrize("shape,fmt,emu", [((5, 20000), "fp8e4m3", False), ((3, 40000), "fp16", False),
+                                           ((2, 65536), "fp8e4m3", False), ((2, 17000), "fp8e4m3", True)])
+def test_split_long_rows_cluster(cuda, shape, fmt, emu):
+    """kb > 16384: a cluster of CTAs shares each row (DSMEM max per slice)."""
+    import oracle
+
+    oz = _oz()
+    rng = np.random.default_rng(shape[1])
+    X = spread_matrix(rng, *shape, 1.0)
+    params = oz.compute_params(53, oz.get_format(fmt).mant_bits, 24, shape[1])
+    ss = oz.slice_matrix(X, "rows", oz.get_format(fmt), params, "emu" if emu else "fp64")
+    coeff, expo, _, s, flags = oracle.split_rows(X, params.rho, emu)
+    assert flags == 0 and ss.s == s
+    for p in range(s):
+        assert np.array_equal(bits(ss.coeff[p]), bits(coeff[p])), f"coeff plane {p}"
+        assert np.array_equal(ss.expo[p], expo[p].astype(np.int64)), f"expo plane {p}"
+
+
+@pytest.mark.parametrize("emu", [False, True])
+def test_split_plane_cap_fallback(cuda, emu, monkeypatch):
+    """Rows needing more planes than the one-pass buffer holds re-run the exact
+    two-pass split; the result is unchanged."""
+    import oracle
+    from paper_2508_00441_b200 import slicing
+
+    oz = _oz()
+    monkeypatch.setattr(slicing, "PLANE_CAP", 3)
+    monkeypatch.setattr(slicing, "PLANE_BUDGET_BYTES", 1)
+    rng = np.random.default_rng(77)
+    X = spread_matrix(rng, 40, 300, 4.0)
+    params = oz.compute_params(53, 4, 24, 300)
+    ss = oz.slice_matrix(X, "rows", oz.get_format("fp8e4m3"), params, "emu" if emu else "fp64")
+    coeff, expo, _, s, flags = oracle.split_rows(X, params.rho, emu)
+    assert s > 3 and ss.s == s
+    for p in range(s):
+        assert np.array_equal(bits(ss.coeff[p]), bits(coeff[p]))
+        assert np.array_equal(ss.expo[p], expo[p].astype(np.int64))
+
+
+def test_oz_gemm_long_k_bitwise(cuda):
+    """k = 20000 > 16384 (cluster split) through the fused pair GEMM."""
+    import oracle
+
+    oz = _oz()
+    rng = np.random.default_rng(20000)
+    A = spread_matrix(rng, 40, 20000, 0.5)
+    B = spread_matrix(rng, 20000, 24, 0.5)
+    cfg = oz.GemmConfig(oz.get_format("fp8e4m3"), oz.get_format("fp32"))
+    res = oz.oz_gemm(A, B, cfg)
+    Cref, info = oracle.oz_gemm(A, B, "fp8e4m3", "fp32")
+    assert info["flags"] == 0
+    assert np.array_equal(bits(res.C), bits(Cref))
