@@ -127,17 +127,19 @@ std::mutex g_table_mu;
 struct TableEntry {
   TableKey key;
   uint32_t* ptr;
+  bool clean;
 };
 TableEntry g_tables[64];
 int g_ntables = 0;
 
-int code_table(int type2, const LpFormat& f, int rho, cudaStream_t st, const uint32_t** out) {
+int code_table(int type2, const LpFormat& f, int rho, cudaStream_t st, const uint32_t** out, int* clean) {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_table_mu);
   for (int i = 0; i < g_ntables; ++i)
     if (g_tables[i].key.dev == dev && g_tables[i].key.type2 == type2 && g_tables[i].key.rho == rho) {
       *out = g_tables[i].ptr;
+      *clean = g_tables[i].clean;
       return OZ_OK;
     }
   if (g_ntables == 64) return OZ_EUNSUPPORTED;
@@ -145,9 +147,19 @@ int code_table(int type2, const LpFormat& f, int rho, cudaStream_t st, const uin
   uint32_t* p = nullptr;
   if (cudaMalloc(&p, sizeof(uint32_t) * (2 * kmax + 1)) != cudaSuccess) return OZ_ECUDA;
   oz::build_code_table_kernel<<<(2 * kmax + 1 + 255) / 256, 256, 0, st>>>(p, kmax, rho, f);
-  if (cudaStreamSynchronize(st) != cudaSuccess) return OZ_ECUDA;
-  g_tables[g_ntables++] = {{dev, type2, rho}, p};
+  uint32_t* h = static_cast<uint32_t*>(malloc(sizeof(uint32_t) * (2 * kmax + 1)));
+  if (!h) return OZ_ECUDA;
+  if (cudaMemcpyAsync(h, p, sizeof(uint32_t) * (2 * kmax + 1), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    free(h);
+    return OZ_ECUDA;
+  }
+  bool ok = true;
+  for (int i = 0; i <= 2 * kmax; ++i) ok = ok && !(h[i] >> 16);
+  free(h);
+  g_tables[g_ntables++] = {{dev, type2, rho}, p, ok};
   *out = p;
+  *clean = ok;
   return OZ_OK;
 }
 
@@ -211,7 +223,7 @@ int oz_split_fused(const double* X, int64_t rows, int64_t kb, int64_t ldx, int t
   P.X = X; P.rows = rows; P.kb = kb; P.ldx = ldx; P.rho = rho; P.cap = cap;
   P.coeff = static_cast<uint8_t*>(coeff); P.ld = ld_coeff; P.expo = expo; P.row_cnt = row_cnt;
   P.s_max = s_max; P.flags = flags; P.kmax = 1 << (53 - rho);
-  int rc = code_table(type2, f, rho, st, &P.table);
+  int rc = code_table(type2, f, rho, st, &P.table, &P.table_clean);
   if (rc) return rc;
   if (f.bytes == 1) return emu ? launch_fused_cfg<1, true>(P, st) : launch_fused_cfg<1, false>(P, st);
   return emu ? launch_fused_cfg<2, true>(P, st) : launch_fused_cfg<2, false>(P, st);
@@ -330,6 +342,8 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   if (const char* e = getenv("OZ_TILE_N")) tn = (atoi(e) == 192 && cta == 2 && sy <= oz::PairCfg<2, 192>::kMaxSy) ? 192 : 128;
   if (sy > oz::PairCfg<2, 128>::kMaxSy) return OZ_ESLICES;
   if (const char* e = getenv("OZ_DEBUG_MODE")) P.debug = atoi(e);
+  P.prefetch = 0;  // measured slower at 8..64 k-blocks (extra TMA requests); kept for experiments
+  if (const char* e = getenv("OZ_PREFETCH")) P.prefetch = atoi(e);
   CUtensorMap ma, mb;
   int rc = make_plane_map(&ma, a_planes, f.bytes, kb, m, planes_a, ld_a, oz::kPM);
   if (rc) return rc;

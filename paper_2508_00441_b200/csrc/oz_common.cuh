@@ -253,4 +253,59 @@ OZ_DEVICE uint64_t emu_add(uint64_t a, uint64_t b, uint32_t& flags) {
   return (sbig << 63) | ((uint64_t)exp << 52) | (sig & kFracMask);
 }
 
+// IEEE binary64 a + b, round-to-nearest-even, in integer arithmetic, fast path.
+//
+// Why: on sm_100a the FP64 DADD competes with the FP8 tensor-core MMAs of the
+// same SM (measured: the fused pair-GEMM epilogue stalled on the FP64 pipe and
+// the MMA warp waited ~27% of its time for TMEM accumulators to be released),
+// so the epilogue accumulates with integer ALU ops instead.  Bit-identical to
+// __dadd_rn for every input.  The common case — two normal operands whose sum
+// rounds to a normal — is straight-line code; zeros, subnormals, Inf/NaN, exact
+// cancellation and out-of-range results go to the slow path: emu_add (kEmu: the
+// reference's integer emulation, flags on range errors, fp64emu.py:193-251) or
+// __dadd_rn (hardware mode: full IEEE semantics, rare).
+template <bool kEmu>
+__device__ __noinline__ uint64_t slow_add(uint64_t a, uint64_t b, uint32_t* flags) {
+  if constexpr (kEmu) return emu_add(a, b, *flags);
+  else return d2u(__dadd_rn(u2d(a), u2d(b)));
+}
+
+// Branch-free core of fast_add: r = a + b (RNE) unless `slow` is set, in which
+// case r is meaningless and the caller must use slow_add.  Zero operands are
+// handled here (same results as emu_add, fp64emu.py:247-250).
+OZ_DEVICE uint64_t add_nb(uint64_t a, uint64_t b, bool& slow) {
+  const uint64_t ua = a & ~kSign, ub = b & ~kSign;
+  const bool sw = ub > ua;
+  const uint64_t x = sw ? b : a;          // larger magnitude
+  const uint64_t ux = sw ? ub : ua, uy = sw ? ua : ub;
+  const int ex = (int)(ux >> 52), ey = (int)(uy >> 52);
+  const int d = min(ex - ey, 63);         // d > 54 degenerates to a sticky bit: x + y rounds to x
+  const uint64_t mx = ((ux & kFracMask) | kHidden) << 10;  // [2^62, 2^63), 10 guard bits
+  const uint64_t my0 = ((uy & kFracMask) | kHidden) << 10;
+  const uint64_t myd = my0 >> d;
+  const uint64_t my = myd | ((myd << d) != my0 ? 1ull : 0ull);  // aligned, sticky in bit 0
+  uint64_t m = ((a ^ b) >> 63) == 0 ? mx + my : mx - my;
+  const uint32_t c = (uint32_t)(m >> 63);  // carry out of an addition: one right shift, sticky kept
+  m = (m >> c) | (m & c);
+  const int lz = __clzll((long long)m) - 1;  // cancellation in a subtraction: left shift
+  m <<= lz;
+  const int e = ex + (int)c - lz;
+  const uint64_t sig = m >> 10;  // 53 bits with the hidden bit
+  const uint32_t rem = (uint32_t)m & 1023u;
+  const uint32_t up = (rem + ((uint32_t)sig & 1u) + 511u) >> 10;  // RNE on 10 guard bits (sticky folded)
+  const uint64_t r = (x & kSign) | (((uint64_t)(e - 1) << 52) + sig + up);
+  const bool yzero = uy == 0;
+  // Slow: Inf/NaN or subnormal operands; a non-zero result whose exponent may
+  // leave [1, 2045] (under/overflow).  Exact cancellation gives +0 (RNE).
+  slow = ex >= 2047 || (ex == 0 && ux != 0) || (!yzero && (ey == 0 || (m != 0 && (unsigned)(e - 1) >= 2045u)));
+  return yzero ? (ux == 0 ? (a & b & kSign) : x) : (m == 0 ? 0ull : r);
+}
+
+template <bool kEmu>
+OZ_DEVICE uint64_t fast_add(uint64_t a, uint64_t b, uint32_t& flags) {
+  bool slow;
+  const uint64_t r = add_nb(a, b, slow);
+  return slow ? slow_add<kEmu>(a, b, &flags) : r;
+}
+
 }  // namespace oz

@@ -88,9 +88,12 @@ struct PairParams {
   uint32_t* step_ctr;
   int pace_slack;
   int pairs_per_tile;
+  int prefetch;              // L2 prefetch distance in k-blocks (0 = off)
   // Diagnostics only (OZ_DEBUG_MODE): bit 0 = epilogue skips TMEM loads/math,
   // bit 1 = producer stops loading after the first ring fill (stale operands),
-  // bit 2 = MMA issuer ignores the stage barriers (pure issue rate).
+  // bit 2 = MMA issuer ignores the stage barriers (pure issue rate),
+  // bit 3 = register-Cb columns: TMEM loads without the math,
+  // bit 4 = register-Cb columns: math on synthetic G without TMEM loads.
   int debug;
 };
 
@@ -237,29 +240,32 @@ OZ_DEVICE void tile_coords(int tile, int tiles_m, int tiles_n, int& tm, int& tn)
   tn = r / gm;
 }
 
-// T = ldexp(G, e) rebuilt from the FP32 bit pattern of a non-zero G (always a
-// normal FP32: a non-zero multiple of 2^(2(rho-53)) below 2^24).  Returns false
-// when the term is not added: it underflowed to zero the reference's way (HW
-// mode) or left the normal range (flagged).
-OZ_DEVICE bool make_term(uint32_t g, int e, uint64_t& t, uint32_t& flags, bool emu) {
-  const int ex = (int)((g >> 23) & 0xFFu) + (1023 - 127) + e;
-  const uint64_t sign = (uint64_t)(g >> 31) << 63;
-  const uint64_t frac = (uint64_t)(g & 0x7FFFFFu) << 29;
-  if ((unsigned)(ex - 1) < 2046u) {
-    t = sign | ((uint64_t)ex << 52) | frac;
-    return true;
-  }
-  // Out of the normal range: overflow is always an error; in HW mode a total
-  // underflow rounds to +-0 silently (np.ldexp, ozgemm.py:136-139), a subnormal
-  // result is an error.  The emulated scale2 rejects both (fp64emu.py:269-277).
-  if (emu || ex > 2046) {
-    flags |= FLAG_TERM_RANGE;
-    return false;
-  }
-  const int lead = ex - 1023;  // exponent of the leading bit
-  if (lead <= -1076 || (lead == -1075 && frac == 0)) return false;  // rounds to zero
-  flags |= FLAG_TERM_RANGE;
-  return false;
+// L2 prefetch of one TMA box (no shared memory, no barrier).
+OZ_DEVICE void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
+// T = ldexp(G, e) rebuilt from the FP32 bit pattern of G (a multiple of
+// 2^(2(rho-53)) below 2^24, so never FP32-subnormal), branch-free.  Returns +0
+// when G is zero or the term is not added: it underflowed to zero the
+// reference's way (HW mode: np.ldexp, ozgemm.py:136-139) or left the normal
+// range (bad = true; the host raises RangeError, ozgemm.py:137-139, or in
+// emulated mode fp64emu scale2's error, fp64emu.py:269-277).  e1 = e + 1023 - 127.
+template <bool kEmu>
+OZ_DEVICE uint64_t make_term(uint32_t g, int e1, bool& bad) {
+  const int ex = (int)((g >> 23) & 0xFFu) + e1;
+  const bool nz = (g << 1) != 0u;
+  const bool inr = (unsigned)(ex - 1) < 2046u;
+  const uint32_t hi = (g & 0x80000000u) | ((uint32_t)ex << 20) | ((g >> 3) & 0xFFFFFu);
+  const uint64_t t = ((uint64_t)hi << 32) | (uint64_t)(g << 29);
+  // Out of range: overflow always errs; HW mode lets a total underflow round to
+  // +-0 (lead exponent ex-1023 <= -1076, or -1075 with a zero fraction).
+  const bool to_zero = !kEmu && (ex <= -53 || (ex == -52 && (g & 0x7FFFFFu) == 0u));
+  bad |= nz && !inr && !to_zero;
+  return (nz && inr) ? t : 0ull;
 }
 
 // Pair limits for this CTA's 128-row slab (row128) and the tile's kN columns.
@@ -289,6 +295,42 @@ OZ_DEVICE void unit_limits(const PairParams& P, int tm, int tn, int& lp_walk, in
   }
 }
 
+// The producer's load sequence (tile -> pair -> k-block) as a cursor, so a
+// second copy can run ahead of the ring and prefetch operands into L2: ~27% of
+// the slice-panel reads miss L2 and the 7-stage smem ring alone does not cover
+// the DRAM latency (ncu: the MMA warp waited on full stages).
+template <int kCta, int kN>
+struct LoadCursor {
+  int tile, kbi, arow, brow;
+  PairIter pi;
+  bool ok;
+  OZ_DEVICE void open(const PairParams& P, int num_tiles, int num_units, uint32_t crank) {
+    for (; tile < num_tiles; tile += num_units) {
+      int tm, tn, lp, lq;
+      tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
+      unit_limits<kCta, kN>(P, tm, tn, lp, lq);
+      arow = (tm * kCta + (int)crank) * kPM;
+      brow = tn * kN + (int)crank * (kN / kCta);
+      kbi = 0;
+      pi.init(lp, lq, P.order, P.cutoff);
+      if (pi.valid()) {
+        ok = true;
+        return;
+      }
+    }
+    ok = false;
+  }
+  OZ_DEVICE void next(const PairParams& P, int num_kb, int num_tiles, int num_units, uint32_t crank) {
+    if (!ok) return;
+    if (++kbi < num_kb) return;
+    kbi = 0;
+    pi.next();
+    if (pi.valid()) return;
+    tile += num_units;
+    open(P, num_tiles, num_units, crank);
+  }
+};
+
 OZ_DEVICE void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -303,49 +345,55 @@ OZ_DEVICE void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
 
 OZ_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// Add the terms of 16 consecutive G values (one tcgen05.ld chunk) into 16 Cb entries.
-template <bool kEmu, typename Acc>
-OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_row, int ea, Acc* cb, uint32_t& flags) {
+// Add the terms of 16 consecutive G values (one tcgen05.ld chunk) into 16 Cb
+// entries (Cb += T in the reference pair order, ozgemm.py:194-197).  Straight-
+// line code so the 16 independent adds overlap: a branch per element would
+// serialise them on the add latency, and on sm_100a a DADD waits ~10x longer
+// while the tensor cores run (profiles/microbench_side_r01.json).  A zero term
+// adds +0, which leaves Cb unchanged (Cb is never -0: it starts at +0 and exact
+// cancellation gives +0).  Emulated mode: the integer fast_add (straight-line
+// core, emu_add for the rare operands it cannot take).
+template <bool kEmu>
+OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_row, int ea1, uint64_t* cb, uint32_t& flags) {
+  uint64_t t[16];
+  bool bad = false;
   const int4* ebv = reinterpret_cast<const int4*>(eb_row);
 #pragma unroll
   for (int v = 0; v < 4; ++v) {
     const int4 e4 = ebv[v];
-    const int eb4[4] = {e4.x, e4.y, e4.z, e4.w};
+    t[v * 4 + 0] = make_term<kEmu>(g[v * 4 + 0], ea1 + e4.x, bad);
+    t[v * 4 + 1] = make_term<kEmu>(g[v * 4 + 1], ea1 + e4.y, bad);
+    t[v * 4 + 2] = make_term<kEmu>(g[v * 4 + 2], ea1 + e4.z, bad);
+    t[v * 4 + 3] = make_term<kEmu>(g[v * 4 + 3], ea1 + e4.w, bad);
+  }
+  if (bad) flags |= FLAG_TERM_RANGE;
+  if constexpr (!kEmu) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int j = v * 4 + u;
-      const uint32_t gv = g[j];
-      if ((gv << 1) != 0u) {
-        uint64_t t;
-        if (make_term(gv, ea + eb4[u], t, flags, kEmu)) {
-          if constexpr (kEmu)
-            cb[j] = emu_add(cb[j], t, flags);
-          else
-            cb[j] = __dadd_rn(cb[j], u2d(t));
-        }
-      }
-    }
+    for (int j = 0; j < 16; ++j) cb[j] = d2u(__dadd_rn(u2d(cb[j]), u2d(t[j])));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) cb[j] = fast_add<true>(cb[j], t[j], flags);
   }
 }
 
 // C[row, col0 : col0+cnt] = Cb (first block) or C + Cb (ozgemm.py:204-207).
 template <bool kEmu, typename Acc>
 OZ_DEVICE void store_row(const PairParams& P, int row, int col0, const Acc* cb, int cnt, uint32_t& flags) {
-  Acc* crow = reinterpret_cast<Acc*>(P.C + (int64_t)row * P.ldc + col0);
+  Acc* crow = reinterpret_cast<Acc*>(P.C) + (int64_t)row * P.ldc + col0;
   const bool vec = ((P.ldc & 1) == 0) && ((col0 & 1) == 0) && (col0 + cnt <= P.n);
   if (vec) {
-    using Acc2 = typename std::conditional<kEmu, ulonglong2, double2>::type;
+    using Acc2 = ulonglong2;
 #pragma unroll
     for (int j = 0; j < cnt; j += 2) {
       Acc2 v;
       if (P.accumulate) {
         const Acc2 c = *reinterpret_cast<const Acc2*>(crow + j);
         if constexpr (kEmu) {
-          v.x = emu_add(c.x, cb[j], flags);
-          v.y = emu_add(c.y, cb[j + 1], flags);
+          v.x = fast_add<true>(c.x, cb[j], flags);
+          v.y = fast_add<true>(c.y, cb[j + 1], flags);
         } else {
-          v.x = __dadd_rn(c.x, cb[j]);
-          v.y = __dadd_rn(c.y, cb[j + 1]);
+          v.x = d2u(__dadd_rn(u2d(c.x), u2d(cb[j])));
+          v.y = d2u(__dadd_rn(u2d(c.y), u2d(cb[j + 1])));
         }
       } else {
         v.x = cb[j];
@@ -359,10 +407,8 @@ OZ_DEVICE void store_row(const PairParams& P, int row, int col0, const Acc* cb, 
       if (col0 + j < P.n) {
         Acc v = cb[j];
         if (P.accumulate) {
-          if constexpr (kEmu)
-            v = emu_add(crow[j], cb[j], flags);
-          else
-            v = __dadd_rn(crow[j], cb[j]);
+          if constexpr (kEmu) v = fast_add<true>(crow[j], cb[j], flags);
+          else v = d2u(__dadd_rn(u2d(crow[j]), u2d(cb[j])));
         }
         crow[j] = v;
       }
@@ -415,6 +461,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
       if (elect_one()) {
         uint32_t it = 0;
         bool pacing = true;
+        LoadCursor<kCta, kN> pf;  // runs P.prefetch k-blocks ahead of the loads
+        pf.tile = unit;
+        pf.open(P, num_tiles, num_units, crank);
+        for (int i = 0; i < P.prefetch; ++i) pf.next(P, num_kb, num_tiles, num_units, crank);
         for (int tile = unit; tile < num_tiles; tile += num_units) {
           int tm, tn, lp, lq;
           tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
@@ -450,6 +500,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
               if ((P.debug & 2) && it >= (uint32_t)kStages) {  // diagnostics: no memory traffic
                 if (leader) mbar_arrive(&s.full[st]);
                 continue;
+              }
+              if (P.prefetch > 0) {
+                if (pf.ok) {
+                  const int pk = pf.kbi * kb_elems;
+                  tma_prefetch_3d(&map_a, pk, pf.arow, pf.pi.p);
+                  tma_prefetch_3d(&map_b, pk, pf.brow, pf.pi.q());
+                }
+                pf.next(P, num_kb, num_tiles, num_units, crank);
               }
               if constexpr (kCta == 1) {
                 mbar_arrive_expect_tx(&s.full[st], Cfg::kStageBytes);
@@ -526,9 +584,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
       }
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
 
-      // Emulated mode keeps Cb as raw bit patterns: no double-typed value may
-      // exist, or nvcc turns bit tricks into FP64 instructions (e.g. DADD |x|).
-      using Acc = typename std::conditional<kEmu, uint64_t, double>::type;
+      // Cb is kept as raw FP64 bit patterns; in emulated mode no double-typed
+      // value may exist at all, or nvcc turns bit tricks into FP64 instructions.
+      using Acc = uint64_t;
       Acc cb[64];
 #pragma unroll
       for (int j = 0; j < 64; ++j) cb[j] = Acc(0);
@@ -550,14 +608,26 @@ __global__ void __launch_bounds__(kPThreads, 1)
         // p >= lp: this CTA's rows have an all-zero A slice p (the partner needs it):
         // the term is +0, nothing to add.
         if (p < lp && !(P.debug & 1)) {
-          const int ea = row < P.m ? __ldg(P.expo_a + (int64_t)p * P.m + row) : 0;
+          const int ea1 = (row < P.m ? __ldg(P.expo_a + (int64_t)p * P.m + row) : 0) + (1023 - 127);
           const uint32_t gaddr = tmem + lane_base + buf * kN;
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
             uint32_t g[16];
-            tmem_ld16(gaddr + half * 64 + ch * 16, g);
-            tmem_ld_wait();
-            accumulate16<kEmu>(g, &s.eb[q][half * 64 + ch * 16], ea, cb + ch * 16, flags);
+            if (!(P.debug & 16)) {
+              tmem_ld16(gaddr + half * 64 + ch * 16, g);
+              tmem_ld_wait();
+            } else {  // diagnostics: synthetic G, no TMEM reads
+#pragma unroll
+              for (int j = 0; j < 16; ++j) g[j] = 0x3F800000u + (uint32_t)(j + p);
+            }
+            if (!(P.debug & 8)) {
+              accumulate16<kEmu>(g, &s.eb[q][half * 64 + ch * 16], ea1, cb + ch * 16, flags);
+            } else {  // diagnostics: TMEM reads without the accumulation math
+              uint32_t o = 0;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) o |= g[j];
+              asm volatile("" ::"r"(o));
+            }
           }
           if constexpr (kTmHalf > 0) {
 #pragma unroll
@@ -570,13 +640,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
                 const uint64_t b = (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
-                if constexpr (kEmu) c16[j] = b; else c16[j] = u2d(b);
+                c16[j] = b;
               }
-              accumulate16<kEmu>(g, &s.eb[q][128 + half * kTmHalf + ch * 16], ea, c16, flags);
+              accumulate16<kEmu>(g, &s.eb[q][128 + half * kTmHalf + ch * 16], ea1, c16, flags);
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
-                uint64_t b;
-                if constexpr (kEmu) b = c16[j]; else b = d2u(c16[j]);
+                const uint64_t b = c16[j];
                 w[2 * j] = (uint32_t)b;
                 w[2 * j + 1] = (uint32_t)(b >> 32);
               }
@@ -605,8 +674,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           Acc c16[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const uint64_t b = (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
-            if constexpr (kEmu) c16[j] = b; else c16[j] = u2d(b);
+            c16[j] = (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
           }
           if (row < P.m) store_row<kEmu>(P, row, tn * kN + 128 + half * kTmHalf + ch * 16, c16, 16, flags);
         }

@@ -93,6 +93,7 @@ struct FusedSplitParams {
   uint32_t* flags;
   const uint32_t* table;   // [2K+1] code | (not_representable << 16), index k + K
   int kmax;                // K = 2^(53-rho)
+  int table_clean;         // 1: no entry carries the not-representable bit
 };
 
 // table[k + K] = code of k * 2^(rho-53) (| 1<<16 if not representable).
@@ -108,7 +109,7 @@ __global__ void build_code_table_kernel(uint32_t* table, int kmax, int rho, LpFo
 
 OZ_DEVICE uint32_t elem_key(uint64_t x) {
   const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
-  return (hi << 1) | (lo != 0u ? 1u : 0u);
+  return (hi << 1) + min(lo, 1u);  // IMNMX + LEA
 }
 
 OZ_DEVICE void st_cluster_u32(uint32_t* local_addr, uint32_t rank, uint32_t v) {
@@ -127,8 +128,71 @@ OZ_DEVICE uint32_t cluster_ctarank() {
   return r;
 }
 
+// One reference iteration over this thread's elements (slicing.py:162-176):
+// returns the next max key.  kWrite: emit the 16-byte plane vectors; kChecked:
+// per-element subnormal-residual and representability checks (only needed for
+// rows holding inputs below 2^-969, or code tables with unrepresentable entries).
+template <int kThreads, int kEPT, int kEB, bool kEmu, bool kWrite, bool kChecked>
+OZ_DEVICE uint32_t slice_iteration(uint64_t (&x)[kEPT], const uint64_t sigma, const uint32_t* __restrict__ tblc,
+                                   int K, uint8_t* plane, int64_t base, int t, int64_t ld, uint32_t& flags,
+                                   uint32_t& bad) {
+  constexpr int kV = 16 / kEB;
+  constexpr int kChunks = kEPT / kV;
+  uint32_t key = 0;
+#pragma unroll
+  for (int ch = 0; ch < kChunks; ++ch) {
+    uint32_t codes[kV];
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int i = ch * kV + u;
+      uint64_t xs, xn;
+      if constexpr (kEmu) {
+        xs = emu_add(x[i], sigma, flags);
+        const uint64_t v = emu_add(xs, sigma ^ kSign, flags);
+        xn = emu_add(x[i], v ^ kSign, flags);
+      } else {
+        const double xsd = __dadd_rn(u2d(x[i]), u2d(sigma));
+        xs = d2u(xsd);
+        xn = d2u(__dsub_rn(u2d(x[i]), __dsub_rn(xsd, u2d(sigma))));
+      }
+      x[i] = xn;
+      if constexpr (kWrite) {
+        int k = (int)(uint32_t)xs;  // slice integer: coeff = k * 2^(rho-53)
+        if constexpr (kEmu) k = min(max(k, -K), K);  // only reachable after a flagged range error
+        const uint32_t ent = tblc[k];
+        if constexpr (kChecked) bad |= ent;
+        codes[u] = ent;
+      }
+      key = max(key, elem_key(xn));
+      if constexpr (kChecked) {
+        const uint32_t ef = (uint32_t)((xn >> 52) & 0x7FF);
+        if (ef == 0 && (xn << 1) != 0) flags |= FLAG_SUBNORMAL_RESID;
+      }
+    }
+    if constexpr (kWrite) {
+      const int64_t e0 = base + ((int64_t)ch * kThreads + t) * kV;
+      if (e0 < ld) {
+        uint4 w;
+        if constexpr (kEB == 1) {
+          w.x = __byte_perm(__byte_perm(codes[0], codes[1], 0x0040), __byte_perm(codes[2], codes[3], 0x0040), 0x5410);
+          w.y = __byte_perm(__byte_perm(codes[4], codes[5], 0x0040), __byte_perm(codes[6], codes[7], 0x0040), 0x5410);
+          w.z = __byte_perm(__byte_perm(codes[8], codes[9], 0x0040), __byte_perm(codes[10], codes[11], 0x0040), 0x5410);
+          w.w = __byte_perm(__byte_perm(codes[12], codes[13], 0x0040), __byte_perm(codes[14], codes[15], 0x0040), 0x5410);
+        } else {
+          w.x = __byte_perm(codes[0], codes[1], 0x5410);
+          w.y = __byte_perm(codes[2], codes[3], 0x5410);
+          w.z = __byte_perm(codes[4], codes[5], 0x5410);
+          w.w = __byte_perm(codes[6], codes[7], 0x5410);
+        }
+        *reinterpret_cast<uint4*>(plane + e0 * kEB) = w;
+      }
+    }
+  }
+  return key;
+}
+
 template <int kThreads, int kEPT, int kCL, int kEB, bool kEmu>
-__global__ void __launch_bounds__(kThreads) split_fused_kernel(const FusedSplitParams P) {
+__global__ void __launch_bounds__(kThreads, kThreads <= 256 ? 2 : 1) split_fused_kernel(const FusedSplitParams P) {
   constexpr int kV = 16 / kEB;          // elements per 16-byte plane store
   constexpr int kChunks = kEPT / kV;
   constexpr int kWarps = kThreads / 32;
@@ -180,11 +244,14 @@ __global__ void __launch_bounds__(kThreads) split_fused_kernel(const FusedSplitP
   }
 #pragma unroll
   for (int i = 0; i < kEPT; ++i) key = max(key, elem_key(x[i]));
+  // Checked (slow) iterations only if some input of this CTA is tiny or the
+  // table holds unrepresentable codes; the barrier also publishes the table.
+  const bool checked = __syncthreads_or(tiny) || !P.table_clean;
   if constexpr (kCL > 1) cluster_barrier();  // peers running before any DSMEM store
-  else __syncthreads();                      // table visible
 
   const int64_t plane_stride = P.rows * P.ld * kEB;  // bytes
   uint8_t* const row_plane0 = P.coeff + row * P.ld * kEB;
+  const uint32_t* tblc = tbl + K;
   const bool write = P.coeff != nullptr;  // count-only mode otherwise (no planes, no exponents)
   int cnt = 0;
   for (int it = 0;; ++it) {
@@ -221,54 +288,15 @@ __global__ void __launch_bounds__(kThreads) split_fused_kernel(const FusedSplitP
     }
     const uint64_t sigma = ((uint64_t)sig_exp << 52) | (1ull << 51);
     uint8_t* plane = row_plane0 + (int64_t)it * plane_stride;
-    key = 0;
-#pragma unroll
-    for (int ch = 0; ch < kChunks; ++ch) {
-      uint32_t codes[kV];
-#pragma unroll
-      for (int u = 0; u < kV; ++u) {
-        const int i = ch * kV + u;
-        uint64_t xs, v;
-        if constexpr (kEmu) {
-          xs = emu_add(x[i], sigma, flags);
-          v = emu_add(xs, sigma ^ kSign, flags);
-          x[i] = emu_add(x[i], v ^ kSign, flags);
-        } else {
-          const double xsd = __dadd_rn(u2d(x[i]), u2d(sigma));
-          xs = d2u(xsd);
-          v = d2u(__dsub_rn(xsd, u2d(sigma)));
-          x[i] = d2u(__dsub_rn(u2d(x[i]), u2d(v)));
-        }
-        if (write) {
-          int k = (int)(uint32_t)xs;  // slice integer: coeff = k * 2^(rho-53)
-          if constexpr (kEmu) k = min(max(k, -K), K);  // only reachable after a flagged range error
-          const uint32_t ent = tbl[k + K];
-          bad |= ent;
-          codes[u] = ent;
-        }
-        key = max(key, elem_key(x[i]));
-        if (tiny) {
-          const uint32_t ef = (uint32_t)((x[i] >> 52) & 0x7FF);
-          if (ef == 0 && (x[i] << 1) != 0) flags |= FLAG_SUBNORMAL_RESID;
-        }
-      }
-      const int64_t e0 = base + ((int64_t)ch * kThreads + t) * kV;
-      if (write && e0 < P.ld) {
-        uint4 w;
-        if constexpr (kEB == 1) {
-          w.x = __byte_perm(__byte_perm(codes[0], codes[1], 0x0040), __byte_perm(codes[2], codes[3], 0x0040), 0x5410);
-          w.y = __byte_perm(__byte_perm(codes[4], codes[5], 0x0040), __byte_perm(codes[6], codes[7], 0x0040), 0x5410);
-          w.z = __byte_perm(__byte_perm(codes[8], codes[9], 0x0040), __byte_perm(codes[10], codes[11], 0x0040), 0x5410);
-          w.w = __byte_perm(__byte_perm(codes[12], codes[13], 0x0040), __byte_perm(codes[14], codes[15], 0x0040), 0x5410);
-        } else {
-          w.x = __byte_perm(codes[0], codes[1], 0x5410);
-          w.y = __byte_perm(codes[2], codes[3], 0x5410);
-          w.z = __byte_perm(codes[4], codes[5], 0x5410);
-          w.w = __byte_perm(codes[6], codes[7], 0x5410);
-        }
-        *reinterpret_cast<uint4*>(plane + e0 * kEB) = w;
-      }
-    }
+    if (!write)
+      key = slice_iteration<kThreads, kEPT, kEB, kEmu, false, true>(x, sigma, tblc, K, plane, base, t, P.ld,
+                                                                    flags, bad);
+    else if (checked)
+      key = slice_iteration<kThreads, kEPT, kEB, kEmu, true, true>(x, sigma, tblc, K, plane, base, t, P.ld, flags,
+                                                                   bad);
+    else
+      key = slice_iteration<kThreads, kEPT, kEB, kEmu, true, false>(x, sigma, tblc, K, plane, base, t, P.ld,
+                                                                    flags, bad);
     if (write && t == 0 && rank == 0) P.expo[(int64_t)it * P.rows + row] = c;
     ++cnt;
   }

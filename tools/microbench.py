@@ -35,6 +35,18 @@ def main(out=None):
         r = lib.micro_mma_rate(cta, n, 20000)
         res[f"mma_fp8_cta{cta}_n{n}"] = {"macs_per_clk_per_sm": r, "frac_of_8192": r / 8192}
         print(f"mma fp8 cta_group::{cta} N={n}: {r:.0f} MAC/clk/SM ({r / 8192:.2f} of 8192)", flush=True)
+    lib.micro_side.restype = None
+    lib.micro_side.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                               ctypes.POINTER(ctypes.c_double)]
+    mr, sr = ctypes.c_double(), ctypes.c_double()
+    side_iters_by = [0, 20000, 40000, 40000, 1000, 40000]
+    for side, name in enumerate(["none", "dadd", "iadd64", "ffma", "fast_add_int", "imad32"]):
+        si = side_iters_by[side]
+        for mma_iters, side_iters in ((20000, si), (0, si)) if side else ((20000, 0),):
+            lib.micro_side(side, mma_iters, side_iters, ctypes.byref(mr), ctypes.byref(sr))
+            key = f"side_{name}_mma{int(mma_iters > 0)}_side{int(side_iters > 0)}"
+            res[key] = {"mma_macs_per_clk_per_sm": mr.value, "side_ops_per_clk_per_sm": sr.value}
+            print(f"{key}: MMA {mr.value:.0f} MAC/clk/SM, side {sr.value:.2f} op/clk/SM", flush=True)
     if out:
         Path(out).write_text(json.dumps(res, indent=1))
 
