@@ -308,4 +308,37 @@ OZ_DEVICE uint64_t fast_add(uint64_t a, uint64_t b, uint32_t& flags) {
   return slow ? slow_add<kEmu>(a, b, &flags) : r;
 }
 
+// Branchy variant of fast_add (early exits instead of selects).  Measured
+// faster than the straight-line form inside the emulated epilogue, where the
+// ~60-op integer add is issue-bound and the early exits skip work.
+OZ_DEVICE uint64_t fast_add_br(uint64_t a, uint64_t b, uint32_t& flags) {
+  const uint64_t ua = a & ~kSign, ub = b & ~kSign;
+  const bool sw = ub > ua;
+  const uint64_t x = sw ? b : a;
+  const uint64_t ux = sw ? ub : ua, uy = sw ? ua : ub;
+  const int ex = (int)(ux >> 52), ey = (int)(uy >> 52);
+  const int d = ex - ey;
+  if (ey == 0 || ex >= 2047) return slow_add<true>(a, b, &flags);
+  if (d > 54) return x;  // |y| < ulp(x)/4: x + y rounds to x
+  const uint64_t mx = ((ux & kFracMask) | kHidden) << 10;
+  const uint64_t my0 = ((uy & kFracMask) | kHidden) << 10;
+  const uint64_t my = (my0 >> d) | ((my0 >> d) << d != my0 ? 1ull : 0ull);
+  uint64_t m = ((a ^ b) >> 63) == 0 ? mx + my : mx - my;
+  int e;
+  if (m >> 63) {
+    m = (m >> 1) | (m & 1ull);
+    e = ex + 1;
+  } else {
+    if (m == 0) return 0ull;  // exact cancellation -> +0
+    const int lz = __clzll((long long)m) - 1;
+    m <<= lz;
+    e = ex - lz;
+  }
+  if ((unsigned)(e - 1) >= 2045u) return slow_add<true>(a, b, &flags);
+  const uint64_t sig = m >> 10;
+  const uint32_t rem = (uint32_t)m & 1023u;
+  const uint32_t up = (rem + ((uint32_t)sig & 1u) + 511u) >> 10;
+  return (x & kSign) | (((uint64_t)(e - 1) << 52) + sig + up);
+}
+
 }  // namespace oz

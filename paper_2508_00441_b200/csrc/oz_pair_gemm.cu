@@ -25,6 +25,7 @@
 //               in that instantiation, tests/test_capi.py checks the SASS).
 // Producers of all resident CTAs are paced to within `pace_slack` pair-steps of
 // each other so concurrently used slice panels stay L2-resident.
+#include <climits>
 #include <type_traits>
 
 #include "oz_common.cuh"
@@ -49,7 +50,7 @@ struct PairCfg {
   static constexpr int kTmCols = kN - 128;                    // C columns whose Cb lives in TMEM
   static constexpr int kCbTmem = kAccBufs * kN;               // first TMEM column of that Cb
   static constexpr int kMaxSy = kN == 128 ? 48 : 32;          // B-exponent staging cap (planes)
-  static constexpr int kSmemBudget = 227 * 1024 - 2048 - kMaxSy * kN * 4;
+  static constexpr int kSmemBudget = 227 * 1024 - 2048 - kMaxSy * (kN + 2) * 4;
   static constexpr int kStages = kSmemBudget / kStageBytes > 8 ? 8 : kSmemBudget / kStageBytes;
   static_assert(kCbTmem + 2 * kTmCols <= kTmemCols, "TMEM budget");
   static_assert(kN == 128 || kCta == 2, "N > 128 needs the CTA pair");
@@ -60,7 +61,8 @@ struct PairSmem {
   using Cfg = PairCfg<kCta, kN>;
   alignas(1024) uint8_t a[Cfg::kStages][kPM * 128];
   alignas(1024) uint8_t b[Cfg::kStages][Cfg::kBRows * 128];
-  int32_t eb[Cfg::kMaxSy][kN];
+  int32_t eb[Cfg::kMaxSy][kN];       // B exponents of the tile's columns, pre-shifted << 20
+  int32_t eb_min[Cfg::kMaxSy], eb_max[Cfg::kMaxSy];  // per plane, over the tile's columns
   uint64_t full[Cfg::kStages], empty[Cfg::kStages];
   uint64_t acc_full[Cfg::kAccBufs], acc_empty[Cfg::kAccBufs];
   uint32_t tmem_base;
@@ -349,31 +351,72 @@ OZ_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::
 // entries (Cb += T in the reference pair order, ozgemm.py:194-197).  Straight-
 // line code so the 16 independent adds overlap: a branch per element would
 // serialise them on the add latency, and on sm_100a a DADD waits ~10x longer
-// while the tensor cores run (profiles/microbench_side_r01.json).  A zero term
-// adds +0, which leaves Cb unchanged (Cb is never -0: it starts at +0 and exact
-// cancellation gives +0).  Emulated mode: the integer fast_add (straight-line
-// core, emu_add for the rare operands it cannot take).
+// while the tensor cores run (profiles/microbench_r01.txt).  A zero term adds
+// +0, which leaves Cb unchanged (Cb is never -0: it starts at +0 and exact
+// cancellation gives +0).
+//   safe: every term of this (row, pair) is known to be normal (per-pair
+//   exponent bounds), so T = G * 2^(eA+eB) is assembled with 5 integer ops:
+//   FP32 bits >> 3 put G's exponent in the FP64 field, + (eA + eB + 896) << 20
+//   rebiases it (ea_sh, eb_sh pre-shifted), the sign is or-ed back, and the low
+//   word is G << 29.  Otherwise the checked make_term handles range errors.
+//   Emulated mode: integer fast_add (emu_add for the rare operands it cannot take).
 template <bool kEmu>
-OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_row, int ea1, uint64_t* cb, uint32_t& flags) {
+OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_sh, int ea_sh, bool safe, uint64_t* cb,
+                            uint32_t& flags) {
+  const int4* ebv = reinterpret_cast<const int4*>(eb_sh);
+  if constexpr (kEmu) {
+    // Emulated mode: one term + one integer add per element (fewer live
+    // registers than staging 16 terms; the add is ALU-bound anyway).
+    bool bad = false;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int4 e4 = ebv[v];
+      const int e[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t gv = g[v * 4 + u];
+        if ((gv << 1) == 0u) continue;  // G = 0: nothing to add
+        uint64_t t;
+        if (safe) {
+          const uint32_t hi = (((gv >> 3) & 0x0FFFFFFFu) + (uint32_t)(ea_sh + e[u])) | (gv & 0x80000000u);
+          t = ((uint64_t)hi << 32) | (uint64_t)(gv << 29);
+        } else {
+          t = make_term<true>(gv, (ea_sh >> 20) + (e[u] >> 20), bad);
+          if (t == 0) continue;
+        }
+        cb[v * 4 + u] = fast_add_br(cb[v * 4 + u], t, flags);
+      }
+    }
+    if (bad) flags |= FLAG_TERM_RANGE;
+    return;
+  }
   uint64_t t[16];
-  bool bad = false;
-  const int4* ebv = reinterpret_cast<const int4*>(eb_row);
+  if (safe) {
 #pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    const int4 e4 = ebv[v];
-    t[v * 4 + 0] = make_term<kEmu>(g[v * 4 + 0], ea1 + e4.x, bad);
-    t[v * 4 + 1] = make_term<kEmu>(g[v * 4 + 1], ea1 + e4.y, bad);
-    t[v * 4 + 2] = make_term<kEmu>(g[v * 4 + 2], ea1 + e4.z, bad);
-    t[v * 4 + 3] = make_term<kEmu>(g[v * 4 + 3], ea1 + e4.w, bad);
-  }
-  if (bad) flags |= FLAG_TERM_RANGE;
-  if constexpr (!kEmu) {
+    for (int v = 0; v < 4; ++v) {
+      const int4 e4 = ebv[v];
+      const int e[4] = {e4.x, e4.y, e4.z, e4.w};
 #pragma unroll
-    for (int j = 0; j < 16; ++j) cb[j] = d2u(__dadd_rn(u2d(cb[j]), u2d(t[j])));
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t gv = g[v * 4 + u];
+        const uint32_t hi = (((gv >> 3) & 0x0FFFFFFFu) + (uint32_t)(ea_sh + e[u])) | (gv & 0x80000000u);
+        t[v * 4 + u] = ((gv << 1) != 0u) ? (((uint64_t)hi << 32) | (uint64_t)(gv << 29)) : 0ull;
+      }
+    }
   } else {
+    bool bad = false;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) cb[j] = fast_add<true>(cb[j], t[j], flags);
+    for (int v = 0; v < 4; ++v) {
+      const int4 e4 = ebv[v];
+      const int e[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        t[v * 4 + u] = make_term<kEmu>(g[v * 4 + u], (ea_sh >> 20) + (e[u] >> 20), bad);  // eA + eB + 896
+    }
+    if (bad) flags |= FLAG_TERM_RANGE;
   }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) cb[j] = d2u(__dadd_rn(u2d(cb[j]), u2d(t[j])));
 }
 
 // C[row, col0 : col0+cnt] = Cb (first block) or C + Cb (ozgemm.py:204-207).
@@ -580,7 +623,23 @@ __global__ void __launch_bounds__(kPThreads, 1)
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
       for (int idx = epi_tid; idx < lq * kN; idx += 32 * kEpiWarps) {
         const int q = idx / kN, c = idx % kN, gc = tn * kN + c;
-        s.eb[q][c] = gc < P.n ? __ldg(P.expo_b + (int64_t)q * P.n + gc) : 0;
+        s.eb[q][c] = (gc < P.n ? __ldg(P.expo_b + (int64_t)q * P.n + gc) : 0) * (1 << 20);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      // Per-plane exponent bounds over the tile's columns (one warp per plane).
+      for (int q = (epi_tid >> 5); q < lq; q += kEpiWarps) {
+        int lo = INT_MAX, hi = INT_MIN;
+        for (int c = lane; c < kN; c += 32) {
+          const int e = s.eb[q][c] >> 20;
+          lo = min(lo, e);
+          hi = max(hi, e);
+        }
+        lo = __reduce_min_sync(0xFFFFFFFFu, lo);
+        hi = __reduce_max_sync(0xFFFFFFFFu, hi);
+        if (lane == 0) {
+          s.eb_min[q] = lo;
+          s.eb_max[q] = hi;
+        }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
 
@@ -608,7 +667,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         // p >= lp: this CTA's rows have an all-zero A slice p (the partner needs it):
         // the term is +0, nothing to add.
         if (p < lp && !(P.debug & 1)) {
-          const int ea1 = (row < P.m ? __ldg(P.expo_a + (int64_t)p * P.m + row) : 0) + (1023 - 127);
+          const int ea = row < P.m ? __ldg(P.expo_a + (int64_t)p * P.m + row) : 0;
+          const int ea_sh = (ea + 896) * (1 << 20);
+          // Non-zero G has |G| in [2^-8, 2^17): FP32 exponent field in [119, 143].
+          const bool safe = ea + 896 + s.eb_min[q] + 119 >= 1 && ea + 896 + s.eb_max[q] + 143 <= 2046;
           const uint32_t gaddr = tmem + lane_base + buf * kN;
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
@@ -621,7 +683,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
               for (int j = 0; j < 16; ++j) g[j] = 0x3F800000u + (uint32_t)(j + p);
             }
             if (!(P.debug & 8)) {
-              accumulate16<kEmu>(g, &s.eb[q][half * 64 + ch * 16], ea1, cb + ch * 16, flags);
+              accumulate16<kEmu>(g, &s.eb[q][half * 64 + ch * 16], ea_sh, safe, cb + ch * 16, flags);
             } else {  // diagnostics: TMEM reads without the accumulation math
               uint32_t o = 0;
 #pragma unroll
@@ -642,7 +704,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 const uint64_t b = (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
                 c16[j] = b;
               }
-              accumulate16<kEmu>(g, &s.eb[q][128 + half * kTmHalf + ch * 16], ea1, c16, flags);
+              accumulate16<kEmu>(g, &s.eb[q][128 + half * kTmHalf + ch * 16], ea_sh, safe, c16, flags);
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
                 const uint64_t b = c16[j];

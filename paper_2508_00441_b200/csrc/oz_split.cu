@@ -128,12 +128,48 @@ OZ_DEVICE uint32_t cluster_ctarank() {
   return r;
 }
 
+// Emulated mode, rows without tiny inputs: the reference's three emulated adds
+// (xs = x + sigma, v = xs - sigma, x - v; slicing.py:161-164) have exact results
+// that stay normal (see the residual argument above), so they reduce to the
+// integer k = RNE(x / q), q = 2^g, and the exact residual x - k*q — computed here
+// from x's significand with integer ops only (bit-identical to emu_add's results).
+OZ_DEVICE uint64_t emu_slice_elem(uint64_t x, int g, int& k) {
+  const int ef = (int)((x >> 52) & 0x7FF);
+  if ((x << 1) == 0) {  // +-0: k = 0, residual unchanged
+    k = 0;
+    return x;
+  }
+  const uint64_t M = (x & kFracMask) | kHidden;
+  const int sh = g - ef + 1075;  // right shift putting the q grid at bit 0
+  const bool s = (x >> 63) != 0;
+  if (sh <= 0) {                 // x is on the grid: exact cancellation -> +0
+    const int k0 = (int)(M << -sh);
+    k = s ? -k0 : k0;
+    return 0ull;
+  }
+  if (sh >= 64) {                // |x| < q/2
+    k = 0;
+    return x;
+  }
+  const uint64_t k0 = M >> sh;
+  const uint64_t rem = M & ((1ull << sh) - 1);
+  const uint64_t half = 1ull << (sh - 1);
+  const bool up = rem > half || (rem == half && (k0 & 1));  // ties to even
+  const int kk = (int)(k0 + (up ? 1 : 0));
+  k = s ? -kk : kk;
+  const uint64_t rm = up ? (half * 2 - rem) : rem;  // |residual| in units of ulp(x)
+  if (rm == 0) return 0ull;
+  const uint64_t rs = (uint64_t)(up ? !s : s);
+  const int pos = 63 - __clzll((long long)rm);      // <= 52
+  return (rs << 63) | ((uint64_t)(ef + pos - 52) << 52) | ((rm << (52 - pos)) & kFracMask);
+}
+
 // One reference iteration over this thread's elements (slicing.py:162-176):
 // returns the next max key.  kWrite: emit the 16-byte plane vectors; kChecked:
 // per-element subnormal-residual and representability checks (only needed for
 // rows holding inputs below 2^-969, or code tables with unrepresentable entries).
 template <int kThreads, int kEPT, int kEB, bool kEmu, bool kWrite, bool kChecked>
-OZ_DEVICE uint32_t slice_iteration(uint64_t (&x)[kEPT], const uint64_t sigma, const uint32_t* __restrict__ tblc,
+OZ_DEVICE uint32_t slice_iteration(uint64_t (&x)[kEPT], const uint64_t sigma, const int g, const uint32_t* __restrict__ tblc,
                                    int K, uint8_t* plane, int64_t base, int t, int64_t ld, uint32_t& flags,
                                    uint32_t& bad) {
   constexpr int kV = 16 / kEB;
@@ -145,19 +181,22 @@ OZ_DEVICE uint32_t slice_iteration(uint64_t (&x)[kEPT], const uint64_t sigma, co
 #pragma unroll
     for (int u = 0; u < kV; ++u) {
       const int i = ch * kV + u;
-      uint64_t xs, xn;
-      if constexpr (kEmu) {
-        xs = emu_add(x[i], sigma, flags);
+      uint64_t xn;
+      int k;  // slice integer: coeff = k * 2^(rho-53)
+      if constexpr (kEmu && !kChecked) {
+        xn = emu_slice_elem(x[i], g, k);
+      } else if constexpr (kEmu) {
+        const uint64_t xs = emu_add(x[i], sigma, flags);
         const uint64_t v = emu_add(xs, sigma ^ kSign, flags);
         xn = emu_add(x[i], v ^ kSign, flags);
+        k = (int)(uint32_t)xs;
       } else {
         const double xsd = __dadd_rn(u2d(x[i]), u2d(sigma));
-        xs = d2u(xsd);
+        k = (int)(uint32_t)d2u(xsd);
         xn = d2u(__dsub_rn(u2d(x[i]), __dsub_rn(xsd, u2d(sigma))));
       }
       x[i] = xn;
       if constexpr (kWrite) {
-        int k = (int)(uint32_t)xs;  // slice integer: coeff = k * 2^(rho-53)
         if constexpr (kEmu) k = min(max(k, -K), K);  // only reachable after a flagged range error
         const uint32_t ent = tblc[k];
         if constexpr (kChecked) bad |= ent;
@@ -289,13 +328,13 @@ __global__ void __launch_bounds__(kThreads, kThreads <= 256 ? 2 : 1) split_fused
     const uint64_t sigma = ((uint64_t)sig_exp << 52) | (1ull << 51);
     uint8_t* plane = row_plane0 + (int64_t)it * plane_stride;
     if (!write)
-      key = slice_iteration<kThreads, kEPT, kEB, kEmu, false, true>(x, sigma, tblc, K, plane, base, t, P.ld,
+      key = slice_iteration<kThreads, kEPT, kEB, kEmu, false, true>(x, sigma, c + P.rho - 53, tblc, K, plane, base, t, P.ld,
                                                                     flags, bad);
     else if (checked)
-      key = slice_iteration<kThreads, kEPT, kEB, kEmu, true, true>(x, sigma, tblc, K, plane, base, t, P.ld, flags,
+      key = slice_iteration<kThreads, kEPT, kEB, kEmu, true, true>(x, sigma, c + P.rho - 53, tblc, K, plane, base, t, P.ld, flags,
                                                                    bad);
     else
-      key = slice_iteration<kThreads, kEPT, kEB, kEmu, true, false>(x, sigma, tblc, K, plane, base, t, P.ld,
+      key = slice_iteration<kThreads, kEPT, kEB, kEmu, true, false>(x, sigma, c + P.rho - 53, tblc, K, plane, base, t, P.ld,
                                                                     flags, bad);
     if (write && t == 0 && rank == 0) P.expo[(int64_t)it * P.rows + row] = c;
     ++cnt;
