@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=128, help="CPU-baseline sample: rows of C")
     ap.add_argument("--cpu-cols", type=int, default=1024, help="CPU-baseline sample: cols of C")
     ap.add_argument("--acc-rows", type=int, default=256, help="rows of C checked against the DD oracle")
+    ap.add_argument("--no-variants", action="store_true", help="skip the other BASELINE configs (rank 0, N=1)")
     return ap.parse_args()
 
 
@@ -423,9 +424,72 @@ def run_extras(args, torch, oz, A, B, cfg, dev):
                        "oracle": "double-double GEMM (oz_dd_gemm, TwoProd/TwoSum, one final rounding)",
                        "max_rel_err_ozaki": relerr(o), "max_rel_err_cublas_dgemm": relerr(c),
                        "ozaki_vs_cublas_max_abs_diff": float(np.max(np.abs(o - c)))}
+    out["variants"] = run_variants(args, torch, oz, A, B, Cdd, d, nz, c, dev) if not args.no_variants else None
     del C64, Cdd, Coz, C64r
     out["cpu_baseline"] = cpu_baseline(args, args.cpu_rows, args.cpu_cols, n)
     out["cpu_baseline"].pop("blocks", None)
+    return out
+
+
+def _time_steps(torch, oz, A, B, cfg, steps):
+    """Device-timed full oz_gemm steps (split + fused pair GEMM) on resident inputs."""
+    C = torch.empty((A.shape[0], B.shape[1]), dtype=torch.float64, device=A.device)
+    oz.oz_gemm_device(A, B, cfg, out=C)
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e[0].record()
+    for _ in range(steps):
+        _, st = oz.oz_gemm_device(A, B, cfg, out=C)
+    e[1].record()
+    torch.cuda.synchronize()
+    return e[0].elapsed_time(e[1]) / steps, st
+
+
+def run_variants(args, torch, oz, A, B, Cdd, d, nz, c_cublas, dev, steps=3):
+    """The other BASELINE.json configurations at n (rank 0, N=1 leg): FP64-level
+    pair truncation (opt-in extension), integer-emulated accumulation (config 3),
+    FP16 slices with k-blocking at phi = 0.5 and 4 (config 4).  Each: device-
+    timed FP64-equivalent TFLOPS and, where cheap, max rel error vs the DD oracle
+    on the same row sample as the headline."""
+    from paper_2508_00441_b200 import _lib
+
+    n = args.n
+    r = args.acc_rows
+    flops = 2.0 * n ** 3
+    f8, f16, f32 = oz.get_format("fp8e4m3"), oz.get_format("fp16"), oz.get_format("fp32")
+
+    def relerr(X, ref, mask):
+        return float(np.max(np.abs(X[mask] - ref[mask]) / np.abs(ref[mask])))
+
+    def one(name, cfg, A_, B_, dd=None, mask=None, cub=None):
+        ms, st = _time_steps(torch, oz, A_, B_, cfg, steps)
+        row = {"tflops": flops / (ms / 1e3) / 1e12, "ms": ms, "gemm_count": st.gemm_count,
+               "gemm_ops": st.gemm_ops, "blocks": len(st.blocks),
+               "s": [(b.s_x, b.s_y) for b in st.blocks[:1]]}
+        if dd is not None:
+            Co, _ = oz.oz_gemm_device(A_[:r].contiguous(), B_, cfg)
+            row["max_rel_err"] = relerr(Co.cpu().numpy(), dd, mask)
+            if cub is not None:
+                row["max_rel_err_cublas_dgemm"] = cub
+        out[name] = row
+
+    out = {}
+    for cut in (12, 11, 10):
+        one(f"fp8_pair_cutoff_{cut}", oz.GemmConfig(f8, f32, pair_cutoff=cut), A, B, d, nz)
+    one("fp8_emulated_fp64", oz.GemmConfig(f8, f32, fp64_emulation=True), A, B, d, nz)
+    one("fp16_kblock1024_phi0.5", oz.GemmConfig(f16, f32, k_block=1024), A, B, d, nz)
+    # phi = 4 (wide exponent range): new inputs, own DD oracle and cuBLAS error
+    A4, B4 = gpu_inputs(torch, n, n, n, 4.0, 4242, dev)
+    Cdd4 = torch.empty((r, n), dtype=torch.float64, device=dev)
+    _lib.call("oz_dd_gemm", A4[:r].contiguous().data_ptr(), B4.data_ptr(), Cdd4.data_ptr(), r, n, n,
+              _lib.stream_ptr(torch))
+    d4 = Cdd4.cpu().numpy()
+    nz4 = d4 != 0
+    cub4 = relerr(torch.matmul(A4[:r], B4).cpu().numpy(), d4, nz4)
+    one("fp16_kblock1024_phi4", oz.GemmConfig(f16, f32, k_block=1024), A4, B4, d4, nz4, cub4)
+    one("fp8_phi4", oz.GemmConfig(f8, f32), A4, B4, d4, nz4, cub4)
+    one("fp8_phi4_pair_cutoff_12", oz.GemmConfig(f8, f32, pair_cutoff=12), A4, B4, d4, nz4, cub4)
+    del A4, B4, Cdd4
     return out
 
 

@@ -99,14 +99,17 @@ struct PairParams {
   int debug;
 };
 
-OZ_DEVICE uint32_t ld_acquire_gpu(const uint32_t* p) {
+// Pacing counters order nothing (scheduling only), so relaxed accesses suffice:
+// an acquire load costs a CCTL.IVALL (L1 invalidate) per spin and a release
+// reduction a MEMBAR.GPU per pair-step (ncu, profiles/pair_gemm_r01_v4).
+OZ_DEVICE uint32_t ld_relaxed_gpu(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
-OZ_DEVICE void red_release_gpu_add(uint32_t* p, uint32_t v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+OZ_DEVICE void red_relaxed_gpu_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // ───────────── cluster / 2-CTA primitives ─────────────
@@ -528,7 +531,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 const int gw = g / P.pairs_per_tile;
                 const uint32_t need = (uint32_t)(kCta * min(num_units, num_tiles - gw * num_units));
                 const long long t0 = clock64();
-                while (ld_acquire_gpu(P.step_ctr + g) < need) {
+                while (ld_relaxed_gpu(P.step_ctr + g) < need) {
                   __nanosleep(32);
                   if (clock64() - t0 > (1ll << 26)) {
                     pacing = false;
@@ -562,7 +565,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 tma_load_3d_pair(s.b[st], &map_b, &s.full[st], kbi * kb_elems, brow, q, kEvictNormal);
               }
             }
-            if (P.step_ctr) red_release_gpu_add(P.step_ctr + wave * P.pairs_per_tile + t, 1u);
+            if (P.step_ctr) red_relaxed_gpu_add(P.step_ctr + wave * P.pairs_per_tile + t, 1u);
           }
         }
       }
