@@ -30,7 +30,7 @@ import numpy as np
 from . import _lib
 from .errors import DimensionError, SlicingInfeasible
 from .formats import FormatSpec
-from .slicing import compute_params, predict_gemm_count, split_many_device, transpose_device
+from .slicing import compute_params, predict_gemm_count, predict_slice_count, split_many_device, transpose_device
 
 __all__ = [
     "DimensionError", "GemmConfig", "BlockStats", "OzStats", "OzResult", "transpose", "oz_gemm",
@@ -154,6 +154,49 @@ def _as_device(M, torch):
     return torch.from_numpy(np.ascontiguousarray(np.asarray(M, dtype=np.float64))).to("cuda")
 
 
+PANEL_MARGIN_BYTES = 6 << 30  # HBM left free when planning panels
+_TOTAL_MEM = {}
+
+
+def _panel_plan(m: int, n: int, kb: int, eb: int, torch) -> tuple[int, int]:
+    """Rows / columns of C handled per pass.  C[I, J] needs only A's row panel I
+    and B's column panel J (slicing is row/column-local), so when
+    B^T and the slice planes of both operands do not fit next to the caller's
+    A, B, C (n = 65536 on one GPU: ~96 GiB of FP64 plus ~2 x 70 GiB of FP8
+    planes), C is produced panel by panel.  Results are bitwise those of the
+    unpanelled call: a panel whose s is below the global s only lacks all-zero
+    slices, whose terms are +0.  OZ_PANEL_ROWS / OZ_PANEL_COLS force sizes."""
+    mp = int(os.environ.get("OZ_PANEL_ROWS", "0")) or m
+    np_ = int(os.environ.get("OZ_PANEL_COLS", "0")) or n
+    if "OZ_PANEL_ROWS" in os.environ or "OZ_PANEL_COLS" in os.environ:
+        return max(1, min(mp, m)), max(1, min(np_, n))
+    ld = -(-kb // 16) * 16
+    from .slicing import PLANE_CAP, _plane_cap
+
+    pred = predict_slice_count(compute_params(53, 4 if eb == 1 else 11, 24, kb)) or PLANE_CAP
+
+    def planes(rows):  # one-pass buffer, or the two-pass fallback's exact s (<= ~24 at phi <= 4)
+        return max(_plane_cap(rows, ld * eb, pred), 24)
+
+    def need(rows_a, cols_b):  # B^T panel + both operands' slice buffers
+        return (8 * kb * cols_b + planes(cols_b) * cols_b * ld * eb + planes(rows_a) * rows_a * ld * eb
+                + 4 * (rows_a + cols_b) * PLANE_CAP)
+
+    dev = torch.cuda.current_device()
+    if dev not in _TOTAL_MEM:
+        _TOTAL_MEM[dev] = torch.cuda.get_device_properties(dev).total_memory
+    if need(mp, np_) < _TOTAL_MEM[dev] // 4:  # common case: no query, no panels
+        return mp, np_
+    free, _ = torch.cuda.mem_get_info()
+    budget = max(free - PANEL_MARGIN_BYTES, 1 << 30)
+    while need(mp, np_) > budget and (mp > 256 or np_ > 256):
+        if np_ >= mp:
+            np_ = max(256, -(-np_ // 2))
+        else:
+            mp = max(256, -(-mp // 2))
+    return mp, np_
+
+
 def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True):
     """C = A @ B for CUDA float64 tensors; returns (C, OzStats).  No host copies
     of operands or result (the timed hot path of bench.py)."""
@@ -173,6 +216,7 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True):
     flags = torch.zeros(1, dtype=torch.int32, device=A.device)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timing else None
     t_slice = t_gemm = 0.0
+    eb = _lib.ELEM_BYTES.get(cfg.type2.name, 1)
     for bi, (lo, hi) in enumerate(_blocks(k, cfg.k_block)):
         kb = hi - lo
         params = compute_params(53, cfg.type2.mant_bits, cfg.type3.mant_bits, kb)
@@ -180,50 +224,76 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True):
             raise SlicingInfeasible(
                 f"slice width {params.slice_width} < 0 for m2={params.m2}, m3={params.m3}, k={kb}")
         _check_accumulator(params, kb)
-        if timing:
-            ev[0].record()
-        (sa, sb), _ = split_many_device([A[:, lo:hi], transpose_device(B[lo:hi, :])], cfg.type2, params, emu,
-                                        flags_out=flags)
-        if timing:
-            ev[1].record()
-        sx = min(sa.s, cfg.max_slices or sa.s)
-        sy = min(sb.s, cfg.max_slices or sb.s)
+        mp, np_ = _panel_plan(m, n, kb, eb, torch) if m and n else (max(m, 1), max(n, 1))
+        s_a = s_b = 0
+        for j0 in range(0, max(n, 1), np_):
+            j1 = min(n, j0 + np_)
+            for i0 in range(0, max(m, 1), mp):
+                i1 = min(m, i0 + mp)
+                if timing:
+                    ev[0].record()
+                # Row panel of A, column panel of B (columns as K-major rows).  The
+                # reference slices A before B; with panels, B's panel is re-sliced
+                # per A panel only when it changes (j0 loop outside).
+                if i0 == 0:
+                    Bt = transpose_device(B[lo:hi, j0:j1])
+                    (sa, sb), _ = split_many_device([A[i0:i1, lo:hi], Bt], cfg.type2, params, emu,
+                                                    flags_out=flags)
+                else:
+                    (sa,), _ = split_many_device([A[i0:i1, lo:hi]], cfg.type2, params, emu, flags_out=flags)
+                if timing:
+                    ev[1].record()
+                s_a, s_b = max(s_a, sa.s), max(s_b, sb.s)
+                _pair_pass(torch, cfg, sa, sb, i1 - i0, j1 - j0, kb, order, cutoff, emu, bi, C, i0, j0, n,
+                           flags, sp)
+                if timing:
+                    ev[2].record()
+                    ev[2].synchronize()
+                    t_slice += ev[0].elapsed_time(ev[1]) / 1e3
+                    t_gemm += ev[1].elapsed_time(ev[2]) / 1e3
+            del Bt, sb
+        sx = min(s_a, cfg.max_slices or s_a)
+        sy = min(s_b, cfg.max_slices or s_b)
         kept = len(pair_order(sx, sy, cfg.accumulation_order, cfg.pair_cutoff)) \
             if cfg.pair_cutoff is not None else sx * sy
-        stats.slicing_ops += 4 * (sa.s * m * kb + sb.s * kb * n)
+        stats.slicing_ops += 4 * (s_a * m * kb + s_b * kb * n)
         stats.blocks.append(BlockStats(lo, hi, sx, sy, kept))
         stats.gemm_count += kept
         stats.gemm_ops += 2 * m * n * kb * kept
         stats.accum_ops += 2 * m * n * kept + m * n
-        tca = tcb = None
-        if cfg.skip_zero_pairs and m and n:
-            tca = torch.empty((m + 127) // 128, dtype=torch.int32, device=A.device)
-            tcb = torch.empty((n + 127) // 128, dtype=torch.int32, device=A.device)
-            _lib.call("oz_tile_counts", sa.row_cnt.data_ptr(), m, tca.data_ptr(), sp)
-            _lib.call("oz_tile_counts", sb.row_cnt.data_ptr(), n, tcb.data_ptr(), sp)
-        pace = None
-        if tca is None and PACE_SLACK > 0 and m and n:
-            tiles = ((m + 127) // 128) * ((n + 127) // 128)  # upper bound on tile-waves
-            pace = torch.empty(tiles * max(kept, 1), dtype=torch.int32, device=A.device)
-        _lib.call("oz_pair_gemm",
-                  sa.planes.data_ptr() if sa.s else None, sb.planes.data_ptr() if sb.s else None,
-                  sa.ld, sb.ld, sa.s, sb.s,
-                  sa.expo.data_ptr() if sa.s else None, sb.expo.data_ptr() if sb.s else None,
-                  tca.data_ptr() if tca is not None else None,
-                  tcb.data_ptr() if tcb is not None else None,
-                  m, n, kb, sx, sy, _lib.FMT_CODE[cfg.type2.name], order, cutoff, int(emu),
-                  int(bi > 0), C.data_ptr(), n, flags.data_ptr(),
-                  pace.data_ptr() if pace is not None else None, pace.numel() * 4 if pace is not None else 0,
-                  PACE_SLACK, sp)
-        if timing:
-            ev[2].record()
-            ev[2].synchronize()
-            t_slice += ev[0].elapsed_time(ev[1]) / 1e3
-            t_gemm += ev[1].elapsed_time(ev[2]) / 1e3
     f = int(flags.item()) & 0xFFFFFFFF
     _lib.raise_for_flags(f, "pair gemm")
     stats.t_slice, stats.t_gemm = t_slice, t_gemm
     return C, stats
+
+
+def _pair_pass(torch, cfg, sa, sb, m, n, kb, order, cutoff, emu, bi, C, i0, j0, ldc, flags, sp):
+    """One fused pair-GEMM launch for the C panel [i0:i0+m, j0:j0+n]."""
+    sx = min(sa.s, cfg.max_slices or sa.s)
+    sy = min(sb.s, cfg.max_slices or sb.s)
+    tca = tcb = None
+    if cfg.skip_zero_pairs and m and n:
+        tca = torch.empty((m + 127) // 128, dtype=torch.int32, device=C.device)
+        tcb = torch.empty((n + 127) // 128, dtype=torch.int32, device=C.device)
+        _lib.call("oz_tile_counts", sa.row_cnt.data_ptr(), m, tca.data_ptr(), sp)
+        _lib.call("oz_tile_counts", sb.row_cnt.data_ptr(), n, tcb.data_ptr(), sp)
+    pace = None
+    if tca is None and PACE_SLACK > 0 and m and n:
+        kept = len(pair_order(sx, sy, cfg.accumulation_order, cfg.pair_cutoff)) if cfg.pair_cutoff is not None \
+            else sx * sy
+        tiles = ((m + 127) // 128) * ((n + 127) // 128)  # upper bound on tile-waves
+        pace = torch.empty(tiles * max(kept, 1), dtype=torch.int32, device=C.device)
+    Cp = C[i0:, j0:] if (i0 or j0) else C
+    _lib.call("oz_pair_gemm",
+              sa.planes.data_ptr() if sa.s else None, sb.planes.data_ptr() if sb.s else None,
+              sa.ld, sb.ld, sa.s, sb.s,
+              sa.expo.data_ptr() if sa.s else None, sb.expo.data_ptr() if sb.s else None,
+              tca.data_ptr() if tca is not None else None,
+              tcb.data_ptr() if tcb is not None else None,
+              m, n, kb, sx, sy, _lib.FMT_CODE[cfg.type2.name], order, cutoff, int(emu),
+              int(bi > 0), Cp.data_ptr(), ldc, flags.data_ptr(),
+              pace.data_ptr() if pace is not None else None, pace.numel() * 4 if pace is not None else 0,
+              PACE_SLACK, sp)
 
 
 def oz_gemm(A, B, cfg: GemmConfig) -> OzResult:
