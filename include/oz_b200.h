@@ -35,7 +35,7 @@ enum {
   OZ_EUNSUPPORTED = 2, /* format/size combination not implemented on sm_100a */
   OZ_ECUDA = 3,        /* CUDA runtime error at launch                        */
   OZ_ETMAP = 4,        /* cuTensorMapEncodeTiled failed                      */
-  OZ_ESLICES = 5       /* more B slices than the epilogue stages (48)         */
+  OZ_ESLICES = 5       /* reserved (earlier versions: slice-count limit)       */
 };
 
 enum { OZ_FMT_E4M3 = 0, OZ_FMT_E5M2 = 1, OZ_FMT_FP16 = 2, OZ_FMT_BF16 = 3 };
@@ -105,16 +105,22 @@ int oz_tile_counts(const int32_t* row_cnt, int64_t rows, int32_t* tile_cnt, void
  *   keeps all pairs (reference semantics); >= 0 keeps p+q <= pair_cutoff
  *   (opt-in extension).  emu: integer-only FP64 epilogue.  accumulate: 0 writes
  *   C = Cb, 1 writes C = C + Cb.
- *   pace_ws / pace_ws_bytes / pace_slack: optional device scratch (4 bytes per
- *   tile-wave per pair) enabling cross-CTA pacing — resident CTAs stay within
- *   pace_slack pair-steps of each other so slice panels are reused from L2
- *   (scheduling only; results are identical).  Ignored when tile_cnt_a != NULL
- *   or pace_slack <= 0. */
+ *   workspace / workspace_bytes: device scratch of at least
+ *   oz_pair_gemm_workspace(m, n, sx, sy, pair_cutoff) bytes (per-tile B
+ *   exponents for the epilogue, then the pacing counters); OZ_EINVAL if smaller
+ *   than the exponent part.  pace_slack > 0 enables cross-CTA pacing — resident
+ *   CTAs stay within pace_slack pair-steps of each other so slice panels are
+ *   reused from L2 (scheduling only; results are identical); ignored when
+ *   tile_cnt_a != NULL or the workspace has no room for the counters. */
 int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64_t ld_b, int planes_a,
                  int planes_b, const int32_t* expo_a, const int32_t* expo_b, const int32_t* tile_cnt_a,
                  const int32_t* tile_cnt_b, int64_t m, int64_t n, int64_t kb, int sx, int sy, int type2,
                  int order, int pair_cutoff, int emu, int accumulate, double* C, int64_t ldc, uint32_t* flags,
-                 void* pace_ws, int64_t pace_ws_bytes, int pace_slack, void* stream);
+                 void* workspace, int64_t workspace_bytes, int pace_slack, void* stream);
+
+/* Bytes of device workspace oz_pair_gemm needs for these sizes (0 if there is
+ * nothing to compute). */
+int64_t oz_pair_gemm_workspace(int64_t m, int64_t n, int sx, int sy, int pair_cutoff);
 
 /* One slice-pair product D (m x n, fp32) = A (m x k) . B (n x k)^T on tcgen05 —
  * replaces lpgemm.lp_gemm (lpgemm.py:93-120) for slice operands (exact). */

@@ -202,9 +202,43 @@ int launch_fused_cfg(const oz::FusedSplitParams& P, cudaStream_t st) {
   return OZ_EUNSUPPORTED;
 }
 
+// Kernel variant and tiling of one fused pair-GEMM call (shared with the
+// workspace query so both agree).
+struct PairPlan {
+  int cta, tn, tiles_m, tiles_n, pairs;
+  size_t eb_bytes, pace_bytes;
+};
+
+PairPlan plan_pair(int64_t m, int64_t n, int sx, int sy, int pair_cutoff) {
+  PairPlan pl{};
+  // CTA pair (cta_group::2) unless the problem has a single 128-row slab; N = 192
+  // columns per pair tile.  OZ_CTA_GROUP=1|2 and OZ_TILE_N=128|192 override
+  // (experiments, tests).
+  pl.cta = m > oz::kPM ? 2 : 1;
+  if (const char* e = getenv("OZ_CTA_GROUP")) pl.cta = atoi(e) == 1 ? 1 : 2;
+  pl.tn = (pl.cta == 2 && n > 128) ? 192 : 128;
+  if (const char* e = getenv("OZ_TILE_N")) pl.tn = (atoi(e) == 192 && pl.cta == 2) ? 192 : 128;
+  pl.tiles_m = (int)((m + oz::kPM * pl.cta - 1) / (oz::kPM * pl.cta));
+  pl.tiles_n = (int)((n + pl.tn - 1) / pl.tn);
+  pl.pairs = 0;
+  for (int p = 0; p < sx; ++p)
+    for (int q = 0; q < sy; ++q)
+      if (pair_cutoff < 0 || p + q <= pair_cutoff) ++pl.pairs;
+  const size_t n_pad = (size_t)pl.tiles_n * pl.tn;
+  pl.eb_bytes = (sizeof(int32_t) * (size_t)sy * (n_pad + 2 * (size_t)pl.tiles_n) + 255) / 256 * 256;
+  pl.pace_bytes = sizeof(uint32_t) * (size_t)pl.tiles_m * pl.tiles_n * (size_t)pl.pairs;
+  return pl;
+}
+
 }  // namespace
 
 extern "C" {
+
+int64_t oz_pair_gemm_workspace(int64_t m, int64_t n, int sx, int sy, int pair_cutoff) {
+  if (m <= 0 || n <= 0 || sx <= 0 || sy <= 0) return 0;
+  const PairPlan pl = plan_pair(m, n, sx, sy, pair_cutoff);
+  return (int64_t)(pl.eb_bytes + pl.pace_bytes);
+}
 
 int oz_split_fused(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2, int rho, int emu, int cap,
                    void* coeff, int64_t ld_coeff, int32_t* expo, int32_t* row_cnt, int32_t* s_max, uint32_t* flags,
@@ -252,7 +286,7 @@ const char* oz_strerror(int status) {
     case OZ_EUNSUPPORTED: return "unsupported format or size on sm_100a";
     case OZ_ECUDA: return "CUDA launch error";
     case OZ_ETMAP: return "cuTensorMapEncodeTiled failed";
-    case OZ_ESLICES: return "too many B slices for the fused epilogue (max 48)";
+    case OZ_ESLICES: return "reserved (no slice-count limit in this version)";
     default: return "unknown status";
   }
 }
@@ -309,7 +343,7 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
                  int planes_b, const int32_t* expo_a, const int32_t* expo_b, const int32_t* tile_cnt_a,
                  const int32_t* tile_cnt_b, int64_t m, int64_t n, int64_t kb, int sx, int sy, int type2,
                  int order, int pair_cutoff, int emu, int accumulate, double* C, int64_t ldc, uint32_t* flags,
-                 void* pace_ws, int64_t pace_ws_bytes, int pace_slack, void* stream) {
+                 void* workspace, int64_t workspace_bytes, int pace_slack, void* stream) {
   LpFormat f;
   uint32_t idf;
   if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
@@ -333,52 +367,47 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   P.C = C; P.ldc = ldc; P.m = (int)m; P.n = (int)n; P.kb = (int)kb; P.sx = sx; P.sy = sy;
   P.order = order; P.cutoff = pair_cutoff; P.accumulate = accumulate;
   P.elem_bytes = f.bytes; P.fmt = idf; P.flags = flags;
-  // CTA pair (cta_group::2) unless the problem has a single 128-row slab; N = 192
-  // columns per pair tile when the B-exponent staging allows it.  OZ_CTA_GROUP=1|2
-  // and OZ_TILE_N=128|192 override (experiments, tests).
-  int cta = m > oz::kPM ? 2 : 1;
-  if (const char* e = getenv("OZ_CTA_GROUP")) cta = atoi(e) == 1 ? 1 : 2;
-  int tn = (cta == 2 && n > 128 && sy <= oz::PairCfg<2, 192>::kMaxSy) ? 192 : 128;
-  if (const char* e = getenv("OZ_TILE_N")) tn = (atoi(e) == 192 && cta == 2 && sy <= oz::PairCfg<2, 192>::kMaxSy) ? 192 : 128;
-  if (sy > oz::PairCfg<2, 128>::kMaxSy) return OZ_ESLICES;
+  const PairPlan pl = plan_pair(m, n, sx, sy, pair_cutoff);
+  const int cta = pl.cta, tn = pl.tn;
+  if (!workspace || (size_t)workspace_bytes < pl.eb_bytes) return OZ_EINVAL;  // see oz_pair_gemm_workspace
   if (const char* e = getenv("OZ_DEBUG_MODE")) P.debug = atoi(e);
   P.prefetch = 0;  // measured slower at 8..64 k-blocks (extra TMA requests); kept for experiments
   if (const char* e = getenv("OZ_PREFETCH")) P.prefetch = atoi(e);
+  P.group = 8;
+  if (const char* e = getenv("OZ_GROUP")) P.group = atoi(e) > 0 ? atoi(e) : 8;
   CUtensorMap ma, mb;
   int rc = make_plane_map(&ma, a_planes, f.bytes, kb, m, planes_a, ld_a, oz::kPM);
   if (rc) return rc;
   rc = make_plane_map(&mb, b_planes, f.bytes, kb, n, planes_b, ld_b, tn / cta);
   if (rc) return rc;
-  P.tiles_m = (int)((m + oz::kPM * cta - 1) / (oz::kPM * cta));
-  P.tiles_n = (int)((n + tn - 1) / tn);
+  P.tiles_m = pl.tiles_m;
+  P.tiles_n = pl.tiles_n;
   const int tiles = P.tiles_m * P.tiles_n;
+  // Per-tile B exponents for the epilogue (first part of the workspace).
+  P.n_pad = P.tiles_n * tn;
+  int32_t* eb_ws = static_cast<int32_t*>(workspace);
+  P.ebsh = eb_ws;
+  P.ebmm = eb_ws + (size_t)sy * P.n_pad;
+  oz::prep_eb_kernel<<<dim3((unsigned)P.tiles_n, (unsigned)sy), tn, 0, st>>>(expo_b, (int)n, tn, P.n_pad, P.tiles_n,
+                                                                         eb_ws, eb_ws + (size_t)sy * P.n_pad);
   // Pacing needs an identical pair sequence in every tile (no skipping) and
-  // scratch counters (one per tile-wave and pair); sized for the largest grid.
+  // scratch counters (one per tile-wave and pair) after the exponents.
   P.step_ctr = nullptr; P.pace_slack = 0; P.pairs_per_tile = 0;
-  if (!tile_cnt_a && pace_ws && pace_slack > 0) {
-    int pairs = 0;
-    for (int p = 0; p < sx; ++p)
-      for (int q = 0; q < sy; ++q)
-        if (pair_cutoff < 0 || p + q <= pair_cutoff) ++pairs;
-    const int waves = tiles;  // upper bound: one unit
-    const size_t need = sizeof(uint32_t) * (size_t)waves * (size_t)pairs;
-    if (pairs > 0 && need <= (size_t)pace_ws_bytes) {
-      cudaMemsetAsync(pace_ws, 0, need, st);
-      P.step_ctr = static_cast<uint32_t*>(pace_ws);
-      P.pace_slack = pace_slack;
-      P.pairs_per_tile = pairs;
-    }
+  if (!tile_cnt_a && pace_slack > 0 && pl.pairs > 0 &&
+      (size_t)workspace_bytes >= pl.eb_bytes + pl.pace_bytes) {
+    uint8_t* pace = static_cast<uint8_t*>(workspace) + pl.eb_bytes;
+    cudaMemsetAsync(pace, 0, pl.pace_bytes, st);
+    P.step_ctr = reinterpret_cast<uint32_t*>(pace);
+    P.pace_slack = pace_slack;
+    P.pairs_per_tile = pl.pairs;
   }
-  if (cta == 1) {
-    if (emu) return launch_pair_fmt<true, 1, 128>(ma, mb, P, tiles, st);
-    return launch_pair_fmt<false, 1, 128>(ma, mb, P, tiles, st);
-  }
-  if (tn == 192) {
-    if (emu) return launch_pair_fmt<true, 2, 192>(ma, mb, P, tiles, st);
-    return launch_pair_fmt<false, 2, 192>(ma, mb, P, tiles, st);
-  }
-  if (emu) return launch_pair_fmt<true, 2, 128>(ma, mb, P, tiles, st);
-  return launch_pair_fmt<false, 2, 128>(ma, mb, P, tiles, st);
+  if (cta == 1)
+    rc = emu ? launch_pair_fmt<true, 1, 128>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 1, 128>(ma, mb, P, tiles, st);
+  else if (tn == 192)
+    rc = emu ? launch_pair_fmt<true, 2, 192>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 2, 192>(ma, mb, P, tiles, st);
+  else
+    rc = emu ? launch_pair_fmt<true, 2, 128>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 2, 128>(ma, mb, P, tiles, st);
+  return rc;
 }
 
 int oz_dd_gemm(const double* A, const double* B, double* C, int64_t m, int64_t n, int64_t k, void* stream) {

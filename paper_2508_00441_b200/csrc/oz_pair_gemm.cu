@@ -49,9 +49,8 @@ struct PairCfg {
   static constexpr int kAccBufs = kN == 128 ? 4 : 2;
   static constexpr int kTmCols = kN - 128;                    // C columns whose Cb lives in TMEM
   static constexpr int kCbTmem = kAccBufs * kN;               // first TMEM column of that Cb
-  static constexpr int kMaxSy = kN == 128 ? 48 : 32;          // B-exponent staging cap (planes)
-  static constexpr int kSmemBudget = 227 * 1024 - 2048 - kMaxSy * (kN + 2) * 4;
-  static constexpr int kStages = kSmemBudget / kStageBytes > 8 ? 8 : kSmemBudget / kStageBytes;
+  static constexpr int kSmemBudget = 227 * 1024 - 2048;
+  static constexpr int kStages = kSmemBudget / kStageBytes > 10 ? 10 : kSmemBudget / kStageBytes;
   static_assert(kCbTmem + 2 * kTmCols <= kTmemCols, "TMEM budget");
   static_assert(kN == 128 || kCta == 2, "N > 128 needs the CTA pair");
 };
@@ -61,8 +60,6 @@ struct PairSmem {
   using Cfg = PairCfg<kCta, kN>;
   alignas(1024) uint8_t a[Cfg::kStages][kPM * 128];
   alignas(1024) uint8_t b[Cfg::kStages][Cfg::kBRows * 128];
-  int32_t eb[Cfg::kMaxSy][kN];       // B exponents of the tile's columns, pre-shifted << 20
-  int32_t eb_min[Cfg::kMaxSy], eb_max[Cfg::kMaxSy];  // per plane, over the tile's columns
   uint64_t full[Cfg::kStages], empty[Cfg::kStages];
   uint64_t acc_full[Cfg::kAccBufs], acc_empty[Cfg::kAccBufs];
   uint32_t tmem_base;
@@ -71,6 +68,9 @@ struct PairSmem {
 struct PairParams {
   const int32_t* expo_a;     // [sx_planes][m]
   const int32_t* expo_b;     // [sy_planes][n]
+  const int32_t* ebsh;       // [sy][n_pad] B exponents pre-shifted << 20 (prep_eb_kernel)
+  const int32_t* ebmm;       // [sy][tiles_n][2] their min / max over each tile's columns
+  int n_pad;                 // tiles_n * kN
   const int32_t* tile_cnt_a; // [m/128] max slice count over the tile's rows (nullable = no skip)
   const int32_t* tile_cnt_b; // [n/128] (128-column groups, whatever kN is)
   double* C;
@@ -91,6 +91,7 @@ struct PairParams {
   int pace_slack;
   int pairs_per_tile;
   int prefetch;              // L2 prefetch distance in k-blocks (0 = off)
+  int group;                 // raster band height in row-tiles
   // Diagnostics only (OZ_DEBUG_MODE): bit 0 = epilogue skips TMEM loads/math,
   // bit 1 = producer stops loading after the first ring fill (stale operands),
   // bit 2 = MMA issuer ignores the stage barriers (pure issue rate),
@@ -233,10 +234,9 @@ struct PairIter {
   }
 };
 
-OZ_DEVICE void tile_coords(int tile, int tiles_m, int tiles_n, int& tm, int& tn) {
-  // Grouped raster: bands of 16 row-tiles walk across the column tiles, so the
+OZ_DEVICE void tile_coords(int tile, int tiles_m, int tiles_n, int G, int& tm, int& tn) {
+  // Grouped raster: bands of G row-tiles walk across the column tiles, so the
   // CTAs resident at one time share A and B k-panels in L2.
-  constexpr int G = 16;
   const int band = tile / (G * tiles_n);
   const int first_m = band * G;
   const int gm = min(G, tiles_m - first_m);
@@ -312,7 +312,7 @@ struct LoadCursor {
   OZ_DEVICE void open(const PairParams& P, int num_tiles, int num_units, uint32_t crank) {
     for (; tile < num_tiles; tile += num_units) {
       int tm, tn, lp, lq;
-      tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
+      tile_coords(tile, P.tiles_m, P.tiles_n, P.group, tm, tn);
       unit_limits<kCta, kN>(P, tm, tn, lp, lq);
       arow = (tm * kCta + (int)crank) * kPM;
       brow = tn * kN + (int)crank * (kN / kCta);
@@ -373,7 +373,7 @@ OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_sh, int e
     bool bad = false;
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      const int4 e4 = ebv[v];
+      const int4 e4 = __ldg(ebv + v);
       const int e[4] = {e4.x, e4.y, e4.z, e4.w};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -397,7 +397,7 @@ OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_sh, int e
   if (safe) {
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      const int4 e4 = ebv[v];
+      const int4 e4 = __ldg(ebv + v);
       const int e[4] = {e4.x, e4.y, e4.z, e4.w};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -410,7 +410,7 @@ OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_sh, int e
     bool bad = false;
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      const int4 e4 = ebv[v];
+      const int4 e4 = __ldg(ebv + v);
       const int e[4] = {e4.x, e4.y, e4.z, e4.w};
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -459,6 +459,34 @@ OZ_DEVICE void store_row(const PairParams& P, int row, int col0, const Acc* cb, 
         crow[j] = v;
       }
     }
+  }
+}
+
+// B exponents for the epilogue, laid out per output tile: ebsh[q][c] = eB_q[c] << 20
+// (0 past n) and ebmm[q][tile] = (min, max) of eB_q over the tile's columns.  One
+// CTA of kN threads per (tile, q).  Read through L1 by the epilogue, so no smem
+// is spent on exponents and any slice count works.
+__global__ void prep_eb_kernel(const int32_t* __restrict__ expo_b, int n, int kn, int n_pad, int tiles_n,
+                               int32_t* __restrict__ ebsh, int32_t* __restrict__ ebmm) {
+  const int tile = blockIdx.x, q = blockIdx.y, c = threadIdx.x, gc = tile * kn + c;
+  const int e = gc < n ? expo_b[(int64_t)q * n + gc] : 0;
+  ebsh[(int64_t)q * n_pad + gc] = e * (1 << 20);
+  __shared__ int lo[32], hi[32];
+  const int wlo = __reduce_min_sync(0xFFFFFFFFu, gc < n ? e : INT_MAX);
+  const int whi = __reduce_max_sync(0xFFFFFFFFu, gc < n ? e : INT_MIN);
+  if ((c & 31) == 0) {
+    lo[c >> 5] = wlo;
+    hi[c >> 5] = whi;
+  }
+  __syncthreads();
+  if (c == 0) {
+    int a = INT_MAX, b = INT_MIN;
+    for (int w = 0; w < kn / 32; ++w) {
+      a = min(a, lo[w]);
+      b = max(b, hi[w]);
+    }
+    ebmm[((int64_t)q * tiles_n + tile) * 2 + 0] = a == INT_MAX ? 0 : a;
+    ebmm[((int64_t)q * tiles_n + tile) * 2 + 1] = b == INT_MIN ? 0 : b;
   }
 }
 
@@ -513,7 +541,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         for (int i = 0; i < P.prefetch; ++i) pf.next(P, num_kb, num_tiles, num_units, crank);
         for (int tile = unit; tile < num_tiles; tile += num_units) {
           int tm, tn, lp, lq;
-          tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
+          tile_coords(tile, P.tiles_m, P.tiles_n, P.group, tm, tn);
           unit_limits<kCta, kN>(P, tm, tn, lp, lq);
           const int wave = tile / num_units;
           const int arow = (tm * kCta + (int)crank) * kPM;
@@ -575,7 +603,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       uint32_t it = 0, acc_it = 0;
       for (int tile = unit; tile < num_tiles; tile += num_units) {
         int tm, tn, lp, lq;
-        tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
+        tile_coords(tile, P.tiles_m, P.tiles_n, P.group, tm, tn);
         unit_limits<kCta, kN>(P, tm, tn, lp, lq);
         PairIter pi;
         for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
@@ -616,36 +644,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint32_t acc_it = 0;
     for (int tile = unit; tile < num_tiles; tile += num_units) {
       int tm, tn, lp, lq;
-      tile_coords(tile, P.tiles_m, P.tiles_n, tm, tn);
+      tile_coords(tile, P.tiles_m, P.tiles_n, P.group, tm, tn);
       const int row128 = tm * kCta + (int)crank;
       tile_limits<kN>(P, row128, tn, lp, lq);
       int lp_walk;  // pairs the MMA issuer walks (unit_limits)
       unit_limits<kCta, kN>(P, tm, tn, lp_walk, lq);
       const int row = row128 * kPM + quad * 32 + lane;
-      // Stage the tile's B exponents (all planes we will touch) in smem.
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-      for (int idx = epi_tid; idx < lq * kN; idx += 32 * kEpiWarps) {
-        const int q = idx / kN, c = idx % kN, gc = tn * kN + c;
-        s.eb[q][c] = (gc < P.n ? __ldg(P.expo_b + (int64_t)q * P.n + gc) : 0) * (1 << 20);
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-      // Per-plane exponent bounds over the tile's columns (one warp per plane).
-      for (int q = (epi_tid >> 5); q < lq; q += kEpiWarps) {
-        int lo = INT_MAX, hi = INT_MIN;
-        for (int c = lane; c < kN; c += 32) {
-          const int e = s.eb[q][c] >> 20;
-          lo = min(lo, e);
-          hi = max(hi, e);
-        }
-        lo = __reduce_min_sync(0xFFFFFFFFu, lo);
-        hi = __reduce_max_sync(0xFFFFFFFFu, hi);
-        if (lane == 0) {
-          s.eb_min[q] = lo;
-          s.eb_max[q] = hi;
-        }
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-
       // Cb is kept as raw FP64 bit patterns; in emulated mode no double-typed
       // value may exist at all, or nvcc turns bit tricks into FP64 instructions.
       using Acc = uint64_t;
@@ -673,7 +677,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
           const int ea = row < P.m ? __ldg(P.expo_a + (int64_t)p * P.m + row) : 0;
           const int ea_sh = (ea + 896) * (1 << 20);
           // Non-zero G has |G| in [2^-8, 2^17): FP32 exponent field in [119, 143].
-          const bool safe = ea + 896 + s.eb_min[q] + 119 >= 1 && ea + 896 + s.eb_max[q] + 143 <= 2046;
+          const int2 mm = __ldg(reinterpret_cast<const int2*>(P.ebmm) + (int64_t)q * P.tiles_n + tn);
+          const bool safe = ea + 896 + mm.x + 119 >= 1 && ea + 896 + mm.y + 143 <= 2046;
+          const int32_t* ebq = P.ebsh + (int64_t)q * P.n_pad + tn * kN;
           const uint32_t gaddr = tmem + lane_base + buf * kN;
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
@@ -686,7 +692,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
               for (int j = 0; j < 16; ++j) g[j] = 0x3F800000u + (uint32_t)(j + p);
             }
             if (!(P.debug & 8)) {
-              accumulate16<kEmu>(g, &s.eb[q][half * 64 + ch * 16], ea_sh, safe, cb + ch * 16, flags);
+              accumulate16<kEmu>(g, ebq + half * 64 + ch * 16, ea_sh, safe, cb + ch * 16, flags);
             } else {  // diagnostics: TMEM reads without the accumulation math
               uint32_t o = 0;
 #pragma unroll
@@ -707,7 +713,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 const uint64_t b = (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
                 c16[j] = b;
               }
-              accumulate16<kEmu>(g, &s.eb[q][128 + half * kTmHalf + ch * 16], ea_sh, safe, c16, flags);
+              accumulate16<kEmu>(g, ebq + 128 + half * kTmHalf + ch * 16, ea_sh, safe, c16, flags);
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
                 const uint64_t b = c16[j];

@@ -277,12 +277,8 @@ def _pair_pass(torch, cfg, sa, sb, m, n, kb, order, cutoff, emu, bi, C, i0, j0, 
         tcb = torch.empty((n + 127) // 128, dtype=torch.int32, device=C.device)
         _lib.call("oz_tile_counts", sa.row_cnt.data_ptr(), m, tca.data_ptr(), sp)
         _lib.call("oz_tile_counts", sb.row_cnt.data_ptr(), n, tcb.data_ptr(), sp)
-    pace = None
-    if tca is None and PACE_SLACK > 0 and m and n:
-        kept = len(pair_order(sx, sy, cfg.accumulation_order, cfg.pair_cutoff)) if cfg.pair_cutoff is not None \
-            else sx * sy
-        tiles = ((m + 127) // 128) * ((n + 127) // 128)  # upper bound on tile-waves
-        pace = torch.empty(tiles * max(kept, 1), dtype=torch.int32, device=C.device)
+    ws_bytes = _lib.load().oz_pair_gemm_workspace(m, n, sx, sy, cutoff) if m and n and sx and sy else 0
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=C.device)
     Cp = C[i0:, j0:] if (i0 or j0) else C
     _lib.call("oz_pair_gemm",
               sa.planes.data_ptr() if sa.s else None, sb.planes.data_ptr() if sb.s else None,
@@ -292,8 +288,7 @@ def _pair_pass(torch, cfg, sa, sb, m, n, kb, order, cutoff, emu, bi, C, i0, j0, 
               tcb.data_ptr() if tcb is not None else None,
               m, n, kb, sx, sy, _lib.FMT_CODE[cfg.type2.name], order, cutoff, int(emu),
               int(bi > 0), Cp.data_ptr(), ldc, flags.data_ptr(),
-              pace.data_ptr() if pace is not None else None, pace.numel() * 4 if pace is not None else 0,
-              PACE_SLACK, sp)
+              ws.data_ptr(), ws_bytes, PACE_SLACK, sp)
 
 
 def oz_gemm(A, B, cfg: GemmConfig) -> OzResult:

@@ -25,7 +25,7 @@ def lib():
 
 def declared_functions():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(oz_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:int|int64_t|const char\*)\s+(oz_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_header_declares_expected_entry_points():
@@ -102,3 +102,11 @@ def test_hw_kernels_do_use_fp64_and_tensor_cores(lib):
     assert re.search(r"UTC[QH]MMA", body), "tcgen05.mma missing"
     assert "UTMALDG" in body, "TMA load missing"
     assert "LDTM" in body, "tcgen05.ld missing"
+
+
+def test_pair_gemm_workspace_query_without_gpu(lib):
+    # pure host arithmetic: exponent table + pacing counters, 0 when nothing to do
+    assert lib.oz_pair_gemm_workspace(0, 128, 3, 3, -1) == 0
+    small = lib.oz_pair_gemm_workspace(256, 192, 4, 4, -1)
+    assert small > 0 and small % 4 == 0
+    assert lib.oz_pair_gemm_workspace(8192, 8192, 16, 17, -1) > lib.oz_pair_gemm_workspace(8192, 8192, 16, 17, 11)
