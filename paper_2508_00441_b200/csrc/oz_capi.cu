@@ -371,9 +371,14 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   const int cta = pl.cta, tn = pl.tn;
   if (!workspace || (size_t)workspace_bytes < pl.eb_bytes) return OZ_EINVAL;  // see oz_pair_gemm_workspace
   if (const char* e = getenv("OZ_DEBUG_MODE")) P.debug = atoi(e);
-  P.prefetch = 0;  // measured slower at 8..64 k-blocks (extra TMA requests); kept for experiments
-  if (const char* e = getenv("OZ_PREFETCH")) P.prefetch = atoi(e);
   P.group = 8;
+  {
+    const uint64_t hints[3] = {oz::kEvictNormal, oz::kEvictFirst, oz::kEvictLast};
+    const char* ha = getenv("OZ_HINT_A");
+    const char* hb = getenv("OZ_HINT_B");
+    P.hint_a = hints[ha ? (atoi(ha) % 3 + 3) % 3 : 0];
+    P.hint_b = hints[hb ? (atoi(hb) % 3 + 3) % 3 : 0];
+  }
   if (const char* e = getenv("OZ_GROUP")) P.group = atoi(e) > 0 ? atoi(e) : 8;
   CUtensorMap ma, mb;
   int rc = make_plane_map(&ma, a_planes, f.bytes, kb, m, planes_a, ld_a, oz::kPM);

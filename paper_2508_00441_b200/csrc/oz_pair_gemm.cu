@@ -90,8 +90,8 @@ struct PairParams {
   uint32_t* step_ctr;
   int pace_slack;
   int pairs_per_tile;
-  int prefetch;              // L2 prefetch distance in k-blocks (0 = off)
   int group;                 // raster band height in row-tiles
+  uint64_t hint_a, hint_b;   // L2 cache policies of the operand loads
   // Diagnostics only (OZ_DEBUG_MODE): bit 0 = epilogue skips TMEM loads/math,
   // bit 1 = producer stops loading after the first ring fill (stale operands),
   // bit 2 = MMA issuer ignores the stage barriers (pure issue rate),
@@ -245,14 +245,6 @@ OZ_DEVICE void tile_coords(int tile, int tiles_m, int tiles_n, int G, int& tm, i
   tn = r / gm;
 }
 
-// L2 prefetch of one TMA box (no shared memory, no barrier).
-OZ_DEVICE void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
-}
-
 // T = ldexp(G, e) rebuilt from the FP32 bit pattern of G (a multiple of
 // 2^(2(rho-53)) below 2^24, so never FP32-subnormal), branch-free.  Returns +0
 // when G is zero or the term is not added: it underflowed to zero the
@@ -299,42 +291,6 @@ OZ_DEVICE void unit_limits(const PairParams& P, int tm, int tn, int& lp_walk, in
     lp_walk = max(lp_walk, lp1);
   }
 }
-
-// The producer's load sequence (tile -> pair -> k-block) as a cursor, so a
-// second copy can run ahead of the ring and prefetch operands into L2: ~27% of
-// the slice-panel reads miss L2 and the 7-stage smem ring alone does not cover
-// the DRAM latency (ncu: the MMA warp waited on full stages).
-template <int kCta, int kN>
-struct LoadCursor {
-  int tile, kbi, arow, brow;
-  PairIter pi;
-  bool ok;
-  OZ_DEVICE void open(const PairParams& P, int num_tiles, int num_units, uint32_t crank) {
-    for (; tile < num_tiles; tile += num_units) {
-      int tm, tn, lp, lq;
-      tile_coords(tile, P.tiles_m, P.tiles_n, P.group, tm, tn);
-      unit_limits<kCta, kN>(P, tm, tn, lp, lq);
-      arow = (tm * kCta + (int)crank) * kPM;
-      brow = tn * kN + (int)crank * (kN / kCta);
-      kbi = 0;
-      pi.init(lp, lq, P.order, P.cutoff);
-      if (pi.valid()) {
-        ok = true;
-        return;
-      }
-    }
-    ok = false;
-  }
-  OZ_DEVICE void next(const PairParams& P, int num_kb, int num_tiles, int num_units, uint32_t crank) {
-    if (!ok) return;
-    if (++kbi < num_kb) return;
-    kbi = 0;
-    pi.next();
-    if (pi.valid()) return;
-    tile += num_units;
-    open(P, num_tiles, num_units, crank);
-  }
-};
 
 OZ_DEVICE void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
@@ -535,10 +491,6 @@ __global__ void __launch_bounds__(kPThreads, 1)
       if (elect_one()) {
         uint32_t it = 0;
         bool pacing = true;
-        LoadCursor<kCta, kN> pf;  // runs P.prefetch k-blocks ahead of the loads
-        pf.tile = unit;
-        pf.open(P, num_tiles, num_units, crank);
-        for (int i = 0; i < P.prefetch; ++i) pf.next(P, num_kb, num_tiles, num_units, crank);
         for (int tile = unit; tile < num_tiles; tile += num_units) {
           int tm, tn, lp, lq;
           tile_coords(tile, P.tiles_m, P.tiles_n, P.group, tm, tn);
@@ -575,22 +527,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 if (leader) mbar_arrive(&s.full[st]);
                 continue;
               }
-              if (P.prefetch > 0) {
-                if (pf.ok) {
-                  const int pk = pf.kbi * kb_elems;
-                  tma_prefetch_3d(&map_a, pk, pf.arow, pf.pi.p);
-                  tma_prefetch_3d(&map_b, pk, pf.brow, pf.pi.q());
-                }
-                pf.next(P, num_kb, num_tiles, num_units, crank);
-              }
               if constexpr (kCta == 1) {
                 mbar_arrive_expect_tx(&s.full[st], Cfg::kStageBytes);
-                tma_load_3d(s.a[st], &map_a, &s.full[st], kbi * kb_elems, arow, p, kEvictNormal);
-                tma_load_3d(s.b[st], &map_b, &s.full[st], kbi * kb_elems, brow, q, kEvictNormal);
+                tma_load_3d(s.a[st], &map_a, &s.full[st], kbi * kb_elems, arow, p, P.hint_a);
+                tma_load_3d(s.b[st], &map_b, &s.full[st], kbi * kb_elems, brow, q, P.hint_b);
               } else {
                 if (leader) mbar_arrive_expect_tx(&s.full[st], 2 * Cfg::kStageBytes);
-                tma_load_3d_pair(s.a[st], &map_a, &s.full[st], kbi * kb_elems, arow, p, kEvictNormal);
-                tma_load_3d_pair(s.b[st], &map_b, &s.full[st], kbi * kb_elems, brow, q, kEvictNormal);
+                tma_load_3d_pair(s.a[st], &map_a, &s.full[st], kbi * kb_elems, arow, p, P.hint_a);
+                tma_load_3d_pair(s.b[st], &map_b, &s.full[st], kbi * kb_elems, brow, q, P.hint_b);
               }
             }
             if (P.step_ctr) red_relaxed_gpu_add(P.step_ctr + wave * P.pairs_per_tile + t, 1u);
