@@ -335,7 +335,7 @@ def main():
 
     extras = {}
     if rank == 0 and not args.no_extras:
-        extras = run_extras(args, torch, oz, A, B, cfg, dev)
+        extras = run_extras(args, torch, oz, A, B, cfg, dev, world)
     # ---- e2e through the public API with host buffers (pinned) ----
     Ah = A.cpu().pin_memory()
     Bh = B.cpu().pin_memory()
@@ -364,12 +364,34 @@ def main():
                "slices": {"s_x": blk.s_x, "s_y": blk.s_y, "gemm_count": st.gemm_count},
                "step_ms": step_ms}
         out.update(extras)
+        out["fp64_level"] = fp64_level_summary(extras)
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def run_extras(args, torch, oz, A, B, cfg, dev):
+def fp64_level_summary(extras):
+    """Fastest measured configuration whose max rel error vs the DD oracle is no
+    worse than native cuBLAS DGEMM's on the same rows (the
+    definition of FP64-level accuracy used here), next to native DGEMM."""
+    acc, var, nat = extras.get("accuracy"), extras.get("variants"), extras.get("native_dgemm")
+    if not acc or not nat:
+        return None
+    bound = acc["max_rel_err_cublas_dgemm"]
+    cands = [("reference defaults", None, acc["max_rel_err_ozaki"])]
+    for name, v in (var or {}).items():
+        if name.startswith("fp8_pair_cutoff_") and "max_rel_err" in v:
+            cands.append((name, v["tflops"], v["max_rel_err"]))
+    ok = [c for c in cands if c[2] <= bound and c[1] is not None]
+    if not ok:
+        return {"config": "reference defaults", "note": "no faster FP64-level variant measured"}
+    name, tf, err = max(ok, key=lambda c: c[1])
+    return {"config": name.replace("fp8_", "") + " (opt-in extension)", "tflops": tf, "max_rel_err": err,
+            "max_rel_err_cublas_dgemm": bound, "native_dgemm_tflops": nat["tflops"],
+            "vs_native_dgemm": tf / nat["tflops"]}
+
+
+def run_extras(args, torch, oz, A, B, cfg, dev, world=1):
     """Accuracy vs the DD oracle, native cuBLAS DGEMM / FP8 on the same GPU,
     and the CPU baseline (rank 0, N=1 leg)."""
     from paper_2508_00441_b200 import _lib
@@ -424,10 +446,13 @@ def run_extras(args, torch, oz, A, B, cfg, dev):
                        "oracle": "double-double GEMM (oz_dd_gemm, TwoProd/TwoSum, one final rounding)",
                        "max_rel_err_ozaki": relerr(o), "max_rel_err_cublas_dgemm": relerr(c),
                        "ozaki_vs_cublas_max_abs_diff": float(np.max(np.abs(o - c)))}
-    out["variants"] = run_variants(args, torch, oz, A, B, Cdd, d, nz, c, dev) if not args.no_variants else None
+    single = world == 1  # variants and the CPU baseline: rank 0 at N = 1 only
+    out["variants"] = run_variants(args, torch, oz, A, B, Cdd, d, nz, c, dev) \
+        if single and not args.no_variants else None
     del C64, Cdd, Coz, C64r
-    out["cpu_baseline"] = cpu_baseline(args, args.cpu_rows, args.cpu_cols, n)
-    out["cpu_baseline"].pop("blocks", None)
+    if single:
+        out["cpu_baseline"] = cpu_baseline(args, args.cpu_rows, args.cpu_cols, n)
+        out["cpu_baseline"].pop("blocks", None)
     return out
 
 
