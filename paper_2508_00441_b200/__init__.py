@@ -8,9 +8,11 @@ ABI of ``include/oz_b200.h``.  There is no CPU fallback: without the built
 library and a CUDA device the compute entry points raise
 ``BackendUnavailable``.
 
+The reference CLI's subcommands (slices-table, gemm, accuracy, verify) run on
+this backend via ``python -m paper_2508_00441_b200.cli`` (same report schema).
 Out of scope (not on the hot path): the scalar FP64-emulation
-API (F64Word, emu_*), cvt/is_representable, the exact rational oracle
-(ref_gemm, exact_gemm, naive_gemm_fp64) and the CLI.
+API (F64Word, emu_*), cvt/is_representable and the exact rational oracle
+(ref_gemm, exact_gemm, naive_gemm_fp64).
 """
 
 __version__ = "0.1.0"

@@ -230,6 +230,14 @@ PairPlan plan_pair(int64_t m, int64_t n, int sx, int sy, int pair_cutoff) {
   return pl;
 }
 
+__global__ void emu_add_batch_kernel(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
+                                     uint64_t* __restrict__ out, int64_t n, int mode, uint32_t* flags) {
+  uint32_t f = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = mode == 0 ? oz::emu_add(a[i], b[i], f) : oz::fast_add<true>(a[i], b[i], f);
+  if (f) atomicOr(flags, f);
+}
+
 }  // namespace
 
 extern "C" {
@@ -413,6 +421,16 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   else
     rc = emu ? launch_pair_fmt<true, 2, 128>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 2, 128>(ma, mb, P, tiles, st);
   return rc;
+}
+
+int oz_emu_add_batch(const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t n, int mode, uint32_t* flags,
+                     void* stream) {
+  if (n < 0 || (mode != 0 && mode != 1)) return OZ_EINVAL;
+  if (n == 0) return OZ_OK;
+  if (!a || !b || !out || !flags) return OZ_EINVAL;
+  const int64_t blocks = (n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096;
+  emu_add_batch_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(a, b, out, n, mode, flags);
+  return launch_status();
 }
 
 int oz_dd_gemm(const double* A, const double* B, double* C, int64_t m, int64_t n, int64_t k, void* stream) {
