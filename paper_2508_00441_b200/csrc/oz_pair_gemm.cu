@@ -94,9 +94,7 @@ struct PairParams {
   uint64_t hint_a, hint_b;   // L2 cache policies of the operand loads
   // Diagnostics only (OZ_DEBUG_MODE): bit 0 = epilogue skips TMEM loads/math,
   // bit 1 = producer stops loading after the first ring fill (stale operands),
-  // bit 2 = MMA issuer ignores the stage barriers (pure issue rate),
-  // bit 3 = register-Cb columns: TMEM loads without the math,
-  // bit 4 = register-Cb columns: math on synthetic G without TMEM loads.
+  // bit 2 = MMA issuer ignores the stage barriers (pure issue rate).
   int debug;
 };
 
@@ -305,6 +303,16 @@ OZ_DEVICE void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
 }
 
 OZ_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// tcgen05.wait::ld that also "defines" the loaded registers, so the compiler
+// cannot schedule their uses above the wait.
+OZ_DEVICE void tmem_ld_wait_regs(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
+}
 
 // Add the terms of 16 consecutive G values (one tcgen05.ld chunk) into 16 Cb
 // entries (Cb += T in the reference pair order, ozgemm.py:194-197).  Straight-
@@ -581,7 +589,6 @@ __global__ void __launch_bounds__(kPThreads, 1)
     constexpr int kTmHalf = Cfg::kTmCols / 2;  // TMEM-resident Cb columns per thread
     const int quad = warp & 3;               // TMEM lane quadrant this warp may access
     const int half = (warp - 4) >> 2;        // register Cb: cols [64h, 64h+64); TMEM Cb: [128 + kTmHalf*h, +kTmHalf)
-    const int epi_tid = threadIdx.x - 128;   // 0..255
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
     const uint32_t cb_tmem = tmem + lane_base + Cfg::kCbTmem + half * 2 * kTmHalf;  // 2 words per FP64
     uint32_t flags = 0;
@@ -625,24 +632,16 @@ __global__ void __launch_bounds__(kPThreads, 1)
           const bool safe = ea + 896 + mm.x + 119 >= 1 && ea + 896 + mm.y + 143 <= 2046;
           const int32_t* ebq = P.ebsh + (int64_t)q * P.n_pad + tn * kN;
           const uint32_t gaddr = tmem + lane_base + buf * kN;
+          // Software-pipelined TMEM reads: chunk ch+1 loads while chunk ch is
+          // accumulated (the wait names the registers so no use is hoisted above it).
+          uint32_t g[2][16];
+          tmem_ld16(gaddr + half * 64, g[0]);
+          tmem_ld_wait_regs(g[0]);
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
-            uint32_t g[16];
-            if (!(P.debug & 16)) {
-              tmem_ld16(gaddr + half * 64 + ch * 16, g);
-              tmem_ld_wait();
-            } else {  // diagnostics: synthetic G, no TMEM reads
-#pragma unroll
-              for (int j = 0; j < 16; ++j) g[j] = 0x3F800000u + (uint32_t)(j + p);
-            }
-            if (!(P.debug & 8)) {
-              accumulate16<kEmu>(g, ebq + half * 64 + ch * 16, ea_sh, safe, cb + ch * 16, flags);
-            } else {  // diagnostics: TMEM reads without the accumulation math
-              uint32_t o = 0;
-#pragma unroll
-              for (int j = 0; j < 16; ++j) o |= g[j];
-              asm volatile("" ::"r"(o));
-            }
+            if (ch + 1 < 4) tmem_ld16(gaddr + half * 64 + (ch + 1) * 16, g[(ch + 1) & 1]);
+            accumulate16<kEmu>(g[ch & 1], ebq + half * 64 + ch * 16, ea_sh, safe, cb + ch * 16, flags);
+            if (ch + 1 < 4) tmem_ld_wait_regs(g[(ch + 1) & 1]);
           }
           if constexpr (kTmHalf > 0) {
 #pragma unroll
