@@ -350,7 +350,8 @@ def main():
     e2e_t = []
     for _ in range(max(1, min(args.steps, 3))):
         t0 = time.perf_counter()
-        r = oz.oz_gemm(Ah, Bh, cfg)
+        r = oz.oz_gemm(Ah, Bh, cfg)  # host tensors in -> host C out (H2D A, B and D2H C inside)
+        assert not r.C.is_cuda
         torch.cuda.synchronize()
         e2e_t.append(time.perf_counter() - t0)
         del r

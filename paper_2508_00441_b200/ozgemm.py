@@ -294,9 +294,10 @@ def _pair_pass(torch, cfg, sa, sb, m, n, kb, order, cutoff, emu, bi, C, i0, j0, 
 def oz_gemm(A, B, cfg: GemmConfig) -> OzResult:
     """C = A @ B with FP64 accuracy using only tensor-core slice GEMMs.
 
-    Same contract as ``ozdgemm.oz_gemm`` (ozgemm.py:143-211).  numpy inputs are
-    copied to the GPU and C comes back as a numpy array; CUDA tensors stay on
-    the device and C is a CUDA tensor."""
+    Same contract as ``ozdgemm.oz_gemm`` (ozgemm.py:143-211).  C comes back where
+    the inputs live: numpy in -> numpy out; CPU torch tensors in -> CPU tensor
+    out (pinned when A is pinned, so the device->host copy is a DMA); CUDA
+    tensors in -> CUDA tensor out, no host copies."""
     torch = _lib.require_cuda()
     is_torch = isinstance(A, torch.Tensor) and isinstance(B, torch.Tensor)
     if not is_torch:
@@ -306,7 +307,13 @@ def oz_gemm(A, B, cfg: GemmConfig) -> OzResult:
         raise DimensionError(f"cannot multiply shapes {tuple(A.shape)} and {tuple(B.shape)}")
     Ad, Bd = _as_device(A, torch), _as_device(B, torch)
     C, stats = oz_gemm_device(Ad, Bd, cfg)
-    return OzResult(C if is_torch else C.cpu().numpy(), stats)
+    if not is_torch:
+        return OzResult(C.cpu().numpy(), stats)
+    if A.is_cuda:
+        return OzResult(C, stats)
+    Ch = torch.empty(C.shape, dtype=C.dtype, pin_memory=A.is_pinned())
+    Ch.copy_(C)
+    return OzResult(Ch, stats)
 
 
 def oz_gemm_count(m: int, n: int, k: int, cfg: GemmConfig) -> int:

@@ -104,6 +104,10 @@ def test_device_tensors_roundtrip(cuda):
     r2 = oz.oz_gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), cfg)
     assert isinstance(r2.C, torch.Tensor) and r2.C.is_cuda
     assert np.array_equal(bits(r1.C), bits(r2.C.cpu().numpy()))
+    # host (pinned) torch tensors in -> host tensor out
+    r3 = oz.oz_gemm(torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory(), cfg)
+    assert isinstance(r3.C, torch.Tensor) and not r3.C.is_cuda and r3.C.is_pinned()
+    assert np.array_equal(bits(r1.C), bits(r3.C.numpy()))
 
 
 def test_lp_gemm_exact_on_slices(cuda):
