@@ -37,17 +37,22 @@ constexpr int kEpiWarps = 8;
 constexpr int kPThreads = 128 + 32 * kEpiWarps;
 constexpr int kTmemCols = 512;             // whole TMEM: accumulators (+ part of Cb for N > 128)
 
-// kN = output columns per CTA (and MMA N).  N = 128: Cb fully in registers,
-// 4 TMEM accumulators.  N = 192 (cta_group::2 only): 2 accumulators of 192
-// columns; Cb columns [0,128) in registers, [128,192) as FP64 in TMEM columns
-// [384, 512).  N = 192 runs the tensor core at 98% of peak vs 87% for N = 128
-// (profiles/microbench_r01.txt) and reads 25% fewer operand bytes per flop.
-template <int kCta, int kN>
+// kN = output columns per CTA (and MMA N).  Hardware-FP64 mode: N = 128 keeps Cb
+// fully in registers with 4 TMEM accumulators; N = 192 (cta_group::2 only) has 2
+// accumulators of 192 columns, Cb columns [0,128) in registers and [128,192) as
+// FP64 in TMEM columns [384, 512) — the tensor core runs at 98% of peak vs 87%
+// for N = 128 (profiles/microbench_r01.txt) and reads 25% fewer operand bytes per
+// flop.  Emulated mode (N = 128): Cb entirely in TMEM (2 accumulators + 256
+// columns of FP64), so the ~60-op integer add is instantiated once in a rolled
+// chunk loop — fully unrolled over 64 register columns it overflowed the
+// instruction cache (ncu: "no instruction" was the top stall).
+template <int kCta, int kN, bool kEmu>
 struct PairCfg {
   static constexpr int kBRows = kN / kCta;                    // B rows staged per CTA
   static constexpr int kStageBytes = (kPM + kBRows) * 128;    // per CTA
-  static constexpr int kAccBufs = kN == 128 ? 4 : 2;
-  static constexpr int kTmCols = kN - 128;                    // C columns whose Cb lives in TMEM
+  static constexpr int kRegCols = kEmu ? 0 : 128;             // C columns whose Cb lives in registers
+  static constexpr int kAccBufs = (kEmu || kN != 128) ? 2 : 4;
+  static constexpr int kTmCols = kN - kRegCols;               // C columns whose Cb lives in TMEM
   static constexpr int kCbTmem = kAccBufs * kN;               // first TMEM column of that Cb
   static constexpr int kSmemBudget = 227 * 1024 - 2048;
   static constexpr int kStages = kSmemBudget / kStageBytes > 10 ? 10 : kSmemBudget / kStageBytes;
@@ -55,9 +60,9 @@ struct PairCfg {
   static_assert(kN == 128 || kCta == 2, "N > 128 needs the CTA pair");
 };
 
-template <int kCta, int kN>
+template <int kCta, int kN, bool kEmu>
 struct PairSmem {
-  using Cfg = PairCfg<kCta, kN>;
+  using Cfg = PairCfg<kCta, kN, kEmu>;
   alignas(1024) uint8_t a[Cfg::kStages][kPM * 128];
   alignas(1024) uint8_t b[Cfg::kStages][Cfg::kBRows * 128];
   uint64_t full[Cfg::kStages], empty[Cfg::kStages];
@@ -332,26 +337,41 @@ OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_sh, int e
                             uint32_t& flags) {
   const int4* ebv = reinterpret_cast<const int4*>(eb_sh);
   if constexpr (kEmu) {
-    // Emulated mode: one term + one integer add per element (fewer live
-    // registers than staging 16 terms; the add is ALU-bound anyway).
+    // Emulated mode: groups of 8 terms added with the branch-free integer core
+    // (independent chains the scheduler can interleave); the rare operands it
+    // cannot take (zero/subnormal/Inf, possible under/overflow) go through
+    // emu_add after the group.
     bool bad = false;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int4 e4 = __ldg(ebv + v);
-      const int e[4] = {e4.x, e4.y, e4.z, e4.w};
+    for (int h = 0; h < 2; ++h) {
+      uint64_t t[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t gv = g[v * 4 + u];
-        if ((gv << 1) == 0u) continue;  // G = 0: nothing to add
-        uint64_t t;
-        if (safe) {
-          const uint32_t hi = (((gv >> 3) & 0x0FFFFFFFu) + (uint32_t)(ea_sh + e[u])) | (gv & 0x80000000u);
-          t = ((uint64_t)hi << 32) | (uint64_t)(gv << 29);
-        } else {
-          t = make_term<true>(gv, (ea_sh >> 20) + (e[u] >> 20), bad);
-          if (t == 0) continue;
+      for (int v = 0; v < 2; ++v) {
+        const int4 e4 = __ldg(ebv + 2 * h + v);
+        const int e[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t gv = g[8 * h + 4 * v + u];
+          if (safe) {
+            const uint32_t hi = (((gv >> 3) & 0x0FFFFFFFu) + (uint32_t)(ea_sh + e[u])) | (gv & 0x80000000u);
+            t[4 * v + u] = ((gv << 1) != 0u) ? (((uint64_t)hi << 32) | (uint64_t)(gv << 29)) : 0ull;
+          } else {
+            t[4 * v + u] = make_term<true>(gv, (ea_sh >> 20) + (e[u] >> 20), bad);
+          }
         }
-        cb[v * 4 + u] = fast_add_br(cb[v * 4 + u], t, flags);
+      }
+      uint32_t slow = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        bool sl;
+        const uint64_t r = add_nb(cb[8 * h + j], t[j], sl);
+        slow |= (uint32_t)(sl && t[j] != 0) << j;  // a zero term leaves Cb as is
+        cb[8 * h + j] = (sl || t[j] == 0) ? cb[8 * h + j] : r;
+      }
+      if (slow) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if ((slow >> j) & 1u) cb[8 * h + j] = slow_add<true>(cb[8 * h + j], t[j], &flags);
       }
     }
     if (bad) flags |= FLAG_TERM_RANGE;
@@ -458,12 +478,12 @@ template <bool kEmu, int kCta, int kElemBytes, int kN>
 __global__ void __launch_bounds__(kPThreads, 1)
     pair_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const PairParams P) {
-  using Cfg = PairCfg<kCta, kN>;
+  using Cfg = PairCfg<kCta, kN, kEmu>;
   constexpr int kStages = Cfg::kStages;
   constexpr int kAccBufs = Cfg::kAccBufs;
   extern __shared__ uint8_t smem_raw[];
-  PairSmem<kCta, kN>& s =
-      *reinterpret_cast<PairSmem<kCta, kN>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  PairSmem<kCta, kN, kEmu>& s =
+      *reinterpret_cast<PairSmem<kCta, kN, kEmu>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x / 32;
   const int lane = (int)lane_id();
   const uint32_t crank = kCta == 2 ? cluster_rank() : 0;  // rank in the CTA pair
@@ -586,9 +606,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
     // ───────── epilogue: ordered FP64 accumulation ─────────
+    constexpr int kRegCols = Cfg::kRegCols;
     constexpr int kTmHalf = Cfg::kTmCols / 2;  // TMEM-resident Cb columns per thread
     const int quad = warp & 3;               // TMEM lane quadrant this warp may access
-    const int half = (warp - 4) >> 2;        // register Cb: cols [64h, 64h+64); TMEM Cb: [128 + kTmHalf*h, +kTmHalf)
+    const int half = (warp - 4) >> 2;        // register Cb: cols [64h, 64h+64); TMEM Cb: [kRegCols + kTmHalf*h, +kTmHalf)
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
     const uint32_t cb_tmem = tmem + lane_base + Cfg::kCbTmem + half * 2 * kTmHalf;  // 2 words per FP64
     uint32_t flags = 0;
@@ -604,9 +625,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
       // Cb is kept as raw FP64 bit patterns; in emulated mode no double-typed
       // value may exist at all, or nvcc turns bit tricks into FP64 instructions.
       using Acc = uint64_t;
-      Acc cb[64];
+      Acc cb[kRegCols > 0 ? 64 : 1];
 #pragma unroll
-      for (int j = 0; j < 64; ++j) cb[j] = Acc(0);
+      for (int j = 0; j < (kRegCols > 0 ? 64 : 1); ++j) cb[j] = Acc(0);
       if constexpr (kTmHalf > 0) {
         uint32_t z[32];
 #pragma unroll
@@ -634,20 +655,22 @@ __global__ void __launch_bounds__(kPThreads, 1)
           const uint32_t gaddr = tmem + lane_base + buf * kN;
           // Software-pipelined TMEM reads: chunk ch+1 loads while chunk ch is
           // accumulated (the wait names the registers so no use is hoisted above it).
-          uint32_t g[2][16];
-          tmem_ld16(gaddr + half * 64, g[0]);
-          tmem_ld_wait_regs(g[0]);
+          if constexpr (kRegCols > 0) {
+            uint32_t g[2][16];
+            tmem_ld16(gaddr + half * 64, g[0]);
+            tmem_ld_wait_regs(g[0]);
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            if (ch + 1 < 4) tmem_ld16(gaddr + half * 64 + (ch + 1) * 16, g[(ch + 1) & 1]);
-            accumulate16<kEmu>(g[ch & 1], ebq + half * 64 + ch * 16, ea_sh, safe, cb + ch * 16, flags);
-            if (ch + 1 < 4) tmem_ld_wait_regs(g[(ch + 1) & 1]);
+            for (int ch = 0; ch < 4; ++ch) {
+              if (ch + 1 < 4) tmem_ld16(gaddr + half * 64 + (ch + 1) * 16, g[(ch + 1) & 1]);
+              accumulate16<kEmu>(g[ch & 1], ebq + half * 64 + ch * 16, ea_sh, safe, cb + ch * 16, flags);
+              if (ch + 1 < 4) tmem_ld_wait_regs(g[(ch + 1) & 1]);
+            }
           }
           if constexpr (kTmHalf > 0) {
-#pragma unroll
+#pragma unroll(kEmu ? 1 : kTmHalf / 16)
             for (int ch = 0; ch < kTmHalf / 16; ++ch) {
               uint32_t g[16], w[32];
-              tmem_ld16(gaddr + 128 + half * kTmHalf + ch * 16, g);
+              tmem_ld16(gaddr + kRegCols + half * kTmHalf + ch * 16, g);
               tmem_ld32(cb_tmem + ch * 32, w);
               tmem_ld_wait();
               Acc c16[16];
@@ -656,7 +679,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 const uint64_t b = (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
                 c16[j] = b;
               }
-              accumulate16<kEmu>(g, ebq + 128 + half * kTmHalf + ch * 16, ea_sh, safe, c16, flags);
+              accumulate16<kEmu>(g, ebq + kRegCols + half * kTmHalf + ch * 16, ea_sh, safe, c16, flags);
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
                 const uint64_t b = c16[j];
@@ -678,9 +701,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
       // C = Cb (first block) or C = C + Cb (ozgemm.py:204-207).  The TMEM reads
       // are warp-collective (.sync.aligned): issue them outside the row guard.
-      if (row < P.m) store_row<kEmu>(P, row, tn * kN + half * 64, cb, 64, flags);
+      if constexpr (kRegCols > 0)
+        if (row < P.m) store_row<kEmu>(P, row, tn * kN + half * 64, cb, 64, flags);
       if constexpr (kTmHalf > 0) {
-#pragma unroll
+#pragma unroll(kEmu ? 1 : kTmHalf / 16)
         for (int ch = 0; ch < kTmHalf / 16; ++ch) {
           uint32_t w[32];
           tmem_ld32(cb_tmem + ch * 32, w);
@@ -690,7 +714,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           for (int j = 0; j < 16; ++j) {
             c16[j] = (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
           }
-          if (row < P.m) store_row<kEmu>(P, row, tn * kN + 128 + half * kTmHalf + ch * 16, c16, 16, flags);
+          if (row < P.m) store_row<kEmu>(P, row, tn * kN + kRegCols + half * kTmHalf + ch * 16, c16, 16, flags);
         }
       }
     }
@@ -702,9 +726,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
   if (warp == 1) tmem_dealloc_g<kCta>(tmem);
 }
 
-template <int kCta, int kN>
+template <int kCta, int kN, bool kEmu>
 size_t pair_gemm_smem_bytes() {
-  return sizeof(PairSmem<kCta, kN>) + 1024;
+  return sizeof(PairSmem<kCta, kN, kEmu>) + 1024;
 }
 
 }  // namespace oz
