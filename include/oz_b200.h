@@ -111,12 +111,20 @@ int oz_tile_counts(const int32_t* row_cnt, int64_t rows, int32_t* tile_cnt, void
  *   than the exponent part.  pace_slack > 0 enables cross-CTA pacing — resident
  *   CTAs stay within pace_slack pair-steps of each other so slice panels are
  *   reused from L2 (scheduling only; results are identical); ignored when
- *   tile_cnt_a != NULL or the workspace has no room for the counters. */
+ *   tile_cnt_a != NULL or the workspace has no room for the counters.
+ *   C_host / ldc_host / copy_stream: optional device->host copy of the finished
+ *   C (pinned host memory, e.g. cudaHostAlloc).  With a copy stream, each row
+ *   band of C is copied as soon as its tiles are final (the kernel counts
+ *   finished tiles per band; the copy stream waits with cuStreamWaitValue32), so
+ *   the transfer overlaps the rest of the GEMM; without one, C is copied on
+ *   `stream` after the kernel.  Call the copy stream's synchronisation before
+ *   reading C_host.  NULL C_host: no copy. */
 int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64_t ld_b, int planes_a,
                  int planes_b, const int32_t* expo_a, const int32_t* expo_b, const int32_t* tile_cnt_a,
                  const int32_t* tile_cnt_b, int64_t m, int64_t n, int64_t kb, int sx, int sy, int type2,
                  int order, int pair_cutoff, int emu, int accumulate, double* C, int64_t ldc, uint32_t* flags,
-                 void* workspace, int64_t workspace_bytes, int pace_slack, void* stream);
+                 void* workspace, int64_t workspace_bytes, int pace_slack, double* C_host, int64_t ldc_host,
+                 void* copy_stream, void* stream);
 
 /* Bytes of device workspace oz_pair_gemm needs for these sizes (0 if there is
  * nothing to compute). */

@@ -41,7 +41,7 @@ SIGNATURES = {
     "oz_transpose": (_I, [_P, _I64, _I64, _I64, _P, _I64, _P]),
     "oz_tile_counts": (_I, [_P, _I64, _P, _P]),
     "oz_pair_gemm": (_I, [_P, _P, _I64, _I64, _I, _I, _P, _P, _P, _P, _I64, _I64, _I64, _I, _I, _I,
-                          _I, _I, _I, _I, _P, _I64, _P, _P, _I64, _I, _P]),
+                          _I, _I, _I, _I, _P, _I64, _P, _P, _I64, _I, _P, _I64, _P, _P]),
     "oz_pair_gemm_workspace": (ctypes.c_int64, [_I64, _I64, _I, _I, _I]),
     "oz_lp_gemm": (_I, [_P, _P, _I64, _I64, _I64, _I64, _I64, _I, _P, _I64, _P]),
     "oz_emu_add_batch": (_I, [_P, _P, _P, _I64, _I, _P, _P]),

@@ -45,6 +45,21 @@ EncodeFn get_encode() {
 }
 
 // 3-D map over slice planes [planes][rows][ld] with a 128-byte x box_rows box, SWIZZLE_128B.
+using StreamWaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+StreamWaitFn get_wait_value() {
+  static StreamWaitFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<StreamWaitFn>(p);
+  });
+  return fn;
+}
+
 int make_plane_map(CUtensorMap* map, const void* base, int elem_bytes, int64_t k, int64_t rows, int64_t planes,
                    int64_t ld, int box_rows = 128) {
   EncodeFn enc = get_encode();
@@ -205,8 +220,8 @@ int launch_fused_cfg(const oz::FusedSplitParams& P, cudaStream_t st) {
 // Kernel variant and tiling of one fused pair-GEMM call (shared with the
 // workspace query so both agree).
 struct PairPlan {
-  int cta, tn, tiles_m, tiles_n, pairs;
-  size_t eb_bytes, pace_bytes;
+  int cta, tn, tiles_m, tiles_n, pairs, group, bands;
+  size_t eb_bytes, band_bytes, pace_bytes;
 };
 
 PairPlan plan_pair(int64_t m, int64_t n, int sx, int sy, int pair_cutoff, int emu) {
@@ -229,6 +244,10 @@ PairPlan plan_pair(int64_t m, int64_t n, int sx, int sy, int pair_cutoff, int em
   const size_t n_pad = (size_t)pl.tiles_n * pl.tn;
   pl.eb_bytes = (sizeof(int32_t) * (size_t)sy * (n_pad + 2 * (size_t)pl.tiles_n) + 255) / 256 * 256;
   pl.pace_bytes = sizeof(uint32_t) * (size_t)pl.tiles_m * pl.tiles_n * (size_t)pl.pairs;
+  pl.group = 8;
+  if (const char* e = getenv("OZ_GROUP")) pl.group = atoi(e) > 0 ? atoi(e) : 8;
+  pl.bands = (pl.tiles_m + pl.group - 1) / pl.group;
+  pl.band_bytes = (sizeof(uint32_t) * (size_t)pl.bands + 255) / 256 * 256;
   return pl;
 }
 
@@ -247,7 +266,7 @@ extern "C" {
 int64_t oz_pair_gemm_workspace(int64_t m, int64_t n, int sx, int sy, int pair_cutoff) {
   if (m <= 0 || n <= 0 || sx <= 0 || sy <= 0) return 0;
   const PairPlan p0 = plan_pair(m, n, sx, sy, pair_cutoff, 0), p1 = plan_pair(m, n, sx, sy, pair_cutoff, 1);
-  const size_t b0 = p0.eb_bytes + p0.pace_bytes, b1 = p1.eb_bytes + p1.pace_bytes;
+  const size_t b0 = p0.eb_bytes + p0.band_bytes + p0.pace_bytes, b1 = p1.eb_bytes + p1.band_bytes + p1.pace_bytes;
   return (int64_t)(b0 > b1 ? b0 : b1);
 }
 
@@ -354,7 +373,8 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
                  int planes_b, const int32_t* expo_a, const int32_t* expo_b, const int32_t* tile_cnt_a,
                  const int32_t* tile_cnt_b, int64_t m, int64_t n, int64_t kb, int sx, int sy, int type2,
                  int order, int pair_cutoff, int emu, int accumulate, double* C, int64_t ldc, uint32_t* flags,
-                 void* workspace, int64_t workspace_bytes, int pace_slack, void* stream) {
+                 void* workspace, int64_t workspace_bytes, int pace_slack, double* C_host, int64_t ldc_host,
+                 void* copy_stream, void* stream) {
   LpFormat f;
   uint32_t idf;
   if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
@@ -370,6 +390,9 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
       if (ldc == n) cudaMemsetAsync(C, 0, sizeof(double) * m * n, st);
       else cudaMemset2DAsync(C, ldc * sizeof(double), 0, n * sizeof(double), m, st);
     }
+    if (C_host && ldc_host >= n)
+      cudaMemcpy2DAsync(C_host, ldc_host * sizeof(double), C, ldc * sizeof(double), n * sizeof(double), m,
+                        cudaMemcpyDeviceToHost, st);
     return launch_status();
   }
   if (!a_planes || !b_planes || !expo_a || !expo_b) return OZ_EINVAL;
@@ -407,15 +430,33 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   oz::prep_eb_kernel<<<dim3((unsigned)P.tiles_n, (unsigned)sy), tn, 0, st>>>(expo_b, (int)n, tn, P.n_pad, P.tiles_n,
                                                                          eb_ws, eb_ws + (size_t)sy * P.n_pad);
   // Pacing needs an identical pair sequence in every tile (no skipping) and
-  // scratch counters (one per tile-wave and pair) after the exponents.
+  // scratch counters (one per tile-wave and pair) after the exponents and the
+  // band counters.
   P.step_ctr = nullptr; P.pace_slack = 0; P.pairs_per_tile = 0;
   if (!tile_cnt_a && pace_slack > 0 && pl.pairs > 0 &&
-      (size_t)workspace_bytes >= pl.eb_bytes + pl.pace_bytes) {
-    uint8_t* pace = static_cast<uint8_t*>(workspace) + pl.eb_bytes;
+      (size_t)workspace_bytes >= pl.eb_bytes + pl.band_bytes + pl.pace_bytes) {
+    uint8_t* pace = static_cast<uint8_t*>(workspace) + pl.eb_bytes + pl.band_bytes;
     cudaMemsetAsync(pace, 0, pl.pace_bytes, st);
     P.step_ctr = reinterpret_cast<uint32_t*>(pace);
     P.pace_slack = pace_slack;
     P.pairs_per_tile = pl.pairs;
+  }
+  // Overlapped device->host copy of C (optional): band counters zeroed on the
+  // copy stream, the kernel waits for that, and per row band the copy stream
+  // waits (cuStreamWaitValue32) for all of the band's tiles, then copies it.
+  P.band_done = nullptr;
+  cudaStream_t cst = (cudaStream_t)copy_stream;
+  StreamWaitFn wait_fn = C_host ? get_wait_value() : nullptr;
+  const bool overlap = C_host && cst && wait_fn && ldc_host >= n &&
+                       (size_t)workspace_bytes >= pl.eb_bytes + pl.band_bytes;
+  if (overlap) {
+    P.band_done = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(workspace) + pl.eb_bytes);
+    cudaMemsetAsync(P.band_done, 0, pl.band_bytes, cst);
+    cudaEvent_t ev;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, cst);
+    cudaStreamWaitEvent(st, ev, 0);
+    cudaEventDestroy(ev);
   }
   if (cta == 1)
     rc = emu ? launch_pair_fmt<true, 1, 128>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 1, 128>(ma, mb, P, tiles, st);
@@ -423,7 +464,22 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
     rc = launch_pair_fmt<false, 2, 192>(ma, mb, P, tiles, st);  // hardware mode only (plan_pair)
   else
     rc = emu ? launch_pair_fmt<true, 2, 128>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 2, 128>(ma, mb, P, tiles, st);
-  return rc;
+  if (rc) return rc;
+  if (C_host) {
+    const int64_t band_rows = (int64_t)pl.group * oz::kPM * cta;
+    for (int b = 0; b < pl.bands; ++b) {
+      const int64_t r0 = b * band_rows, r1 = r0 + band_rows < m ? r0 + band_rows : m;
+      if (overlap) {
+        const int band_tm = (pl.tiles_m - b * pl.group) < pl.group ? pl.tiles_m - b * pl.group : pl.group;
+        const uint32_t expect = (uint32_t)(band_tm * pl.tiles_n * cta);
+        if (wait_fn(cst, reinterpret_cast<CUdeviceptr>(P.band_done + b), expect, 0x0 /* GEQ */) != CUDA_SUCCESS)
+          return OZ_ECUDA;
+      }
+      cudaMemcpy2DAsync(C_host + r0 * ldc_host, ldc_host * sizeof(double), C + r0 * ldc, ldc * sizeof(double),
+                        n * sizeof(double), r1 - r0, cudaMemcpyDeviceToHost, overlap ? cst : st);
+    }
+  }
+  return launch_status();
 }
 
 int oz_emu_add_batch(const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t n, int mode, uint32_t* flags,

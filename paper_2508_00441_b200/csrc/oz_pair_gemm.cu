@@ -97,6 +97,7 @@ struct PairParams {
   int pairs_per_tile;
   int group;                 // raster band height in row-tiles
   uint64_t hint_a, hint_b;   // L2 cache policies of the operand loads
+  uint32_t* band_done;       // [tiles_m / group] finished-tile counters (nullable)
   // Diagnostics only (OZ_DEBUG_MODE): bit 0 = epilogue skips TMEM loads/math,
   // bit 1 = producer stops loading after the first ring fill (stale operands),
   // bit 2 = MMA issuer ignores the stage barriers (pure issue rate).
@@ -715,6 +716,16 @@ __global__ void __launch_bounds__(kPThreads, 1)
             c16[j] = (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
           }
           if (row < P.m) store_row<kEmu>(P, row, tn * kN + kRegCols + half * kTmHalf + ch * 16, c16, 16, flags);
+        }
+      }
+      // Publish "this tile of C is final" per row band, so a copy stream waiting
+      // on the band counter (cuStreamWaitValue32) can move finished bands to the
+      // host while later tiles compute.
+      if (P.band_done) {
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        if (threadIdx.x == 128) {
+          __threadfence_system();
+          atomicAdd(P.band_done + tm / P.group, 1u);
         }
       }
     }

@@ -197,9 +197,12 @@ def _panel_plan(m: int, n: int, kb: int, eb: int, torch) -> tuple[int, int]:
     return mp, np_
 
 
-def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True):
+def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_out=None):
     """C = A @ B for CUDA float64 tensors; returns (C, OzStats).  No host copies
-    of operands or result (the timed hot path of bench.py)."""
+    of operands or result (the timed hot path of bench.py) unless ``host_out`` (a
+    pinned CPU float64 tensor) is given: then C is also copied there, band by band
+    on a side stream while the last block's GEMM still runs (single-panel runs;
+    otherwise after it)."""
     torch = _lib.require_cuda()
     if A.ndim != 2 or B.ndim != 2 or A.shape[1] != B.shape[0]:
         raise DimensionError(f"cannot multiply shapes {tuple(A.shape)} and {tuple(B.shape)}")
@@ -217,6 +220,7 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timing else None
     t_slice = t_gemm = 0.0
     eb = _lib.ELEM_BYTES.get(cfg.type2.name, 1)
+    mp, np_ = m, n
     for bi, (lo, hi) in enumerate(_blocks(k, cfg.k_block)):
         kb = hi - lo
         params = compute_params(53, cfg.type2.mant_bits, cfg.type3.mant_bits, kb)
@@ -244,8 +248,12 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True):
                 if timing:
                     ev[1].record()
                 s_a, s_b = max(s_a, sa.s), max(s_b, sb.s)
+                last = hi == k and j1 == n and i1 == m
+                host = None
+                if host_out is not None and last and mp == m and np_ == n:
+                    host = (host_out, _copy_stream(torch).cuda_stream)
                 _pair_pass(torch, cfg, sa, sb, i1 - i0, j1 - j0, kb, order, cutoff, emu, bi, C, i0, j0, n,
-                           flags, sp)
+                           flags, sp, host)
                 if timing:
                     ev[2].record()
                     ev[2].synchronize()
@@ -261,13 +269,29 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True):
         stats.gemm_count += kept
         stats.gemm_ops += 2 * m * n * kb * kept
         stats.accum_ops += 2 * m * n * kept + m * n
+    if host_out is not None:
+        if mp == m and np_ == n and m and n:
+            _copy_stream(torch).synchronize()
+        else:  # panelled: plain copy after the last panel
+            host_out.copy_(C)
     f = int(flags.item()) & 0xFFFFFFFF
     _lib.raise_for_flags(f, "pair gemm")
     stats.t_slice, stats.t_gemm = t_slice, t_gemm
     return C, stats
 
 
-def _pair_pass(torch, cfg, sa, sb, m, n, kb, order, cutoff, emu, bi, C, i0, j0, ldc, flags, sp):
+_COPY_STREAMS = {}
+
+
+def _copy_stream(torch):
+    """Per-device side stream for the overlapped device->host copy of C."""
+    d = torch.cuda.current_device()
+    if d not in _COPY_STREAMS:
+        _COPY_STREAMS[d] = torch.cuda.Stream(device=d)
+    return _COPY_STREAMS[d]
+
+
+def _pair_pass(torch, cfg, sa, sb, m, n, kb, order, cutoff, emu, bi, C, i0, j0, ldc, flags, sp, host=None):
     """One fused pair-GEMM launch for the C panel [i0:i0+m, j0:j0+n]."""
     sx = min(sa.s, cfg.max_slices or sa.s)
     sy = min(sb.s, cfg.max_slices or sb.s)
@@ -288,7 +312,9 @@ def _pair_pass(torch, cfg, sa, sb, m, n, kb, order, cutoff, emu, bi, C, i0, j0, 
               tcb.data_ptr() if tcb is not None else None,
               m, n, kb, sx, sy, _lib.FMT_CODE[cfg.type2.name], order, cutoff, int(emu),
               int(bi > 0), Cp.data_ptr(), ldc, flags.data_ptr(),
-              ws.data_ptr(), ws_bytes, PACE_SLACK, sp)
+              ws.data_ptr(), ws_bytes, PACE_SLACK,
+              host[0].data_ptr() if host else None, host[0].shape[1] if host else 0,
+              host[1] if host else None, sp)
 
 
 def oz_gemm(A, B, cfg: GemmConfig) -> OzResult:
@@ -306,14 +332,13 @@ def oz_gemm(A, B, cfg: GemmConfig) -> OzResult:
     if A.ndim != 2 or B.ndim != 2 or A.shape[1] != B.shape[0]:
         raise DimensionError(f"cannot multiply shapes {tuple(A.shape)} and {tuple(B.shape)}")
     Ad, Bd = _as_device(A, torch), _as_device(B, torch)
-    C, stats = oz_gemm_device(Ad, Bd, cfg)
-    if not is_torch:
-        return OzResult(C.cpu().numpy(), stats)
-    if A.is_cuda:
+    if is_torch and A.is_cuda:
+        C, stats = oz_gemm_device(Ad, Bd, cfg)
         return OzResult(C, stats)
-    Ch = torch.empty(C.shape, dtype=C.dtype, pin_memory=A.is_pinned())
-    Ch.copy_(C)
-    return OzResult(Ch, stats)
+    # Host result: pinned buffer filled by the overlapped band copies.
+    Ch = torch.empty((A.shape[0], B.shape[1]), dtype=torch.float64, pin_memory=True)
+    _, stats = oz_gemm_device(Ad, Bd, cfg, host_out=Ch)
+    return OzResult(Ch if is_torch else Ch.numpy(), stats)
 
 
 def oz_gemm_count(m: int, n: int, k: int, cfg: GemmConfig) -> int:
