@@ -66,9 +66,11 @@ int oz_split_fused(const double* X, int64_t rows, int64_t kb, int64_t ldx, int t
 
 /* Zero slices for rows exhausted before the global s (slicing.py:149-152): for
  * every row r, planes [row_cnt[r], s) of coeff[.][rows][ld_coeff] are zeroed and
- * their exponents set to 0.  Completes oz_split_fused. */
+ * their exponents set to 0.  Completes oz_split_fused.  s_dev (nullable): read s
+ * from device memory (oz_split_fused's s_max word) instead, capped at `s` (the
+ * planes allocated) — no host round trip. */
 int oz_split_pad(void* coeff, int64_t ld_coeff, int64_t rows, int type2, int s, int32_t* expo,
-                 const int32_t* row_cnt, void* stream);
+                 const int32_t* row_cnt, const int32_t* s_dev, void* stream);
 
 /* Count pass of the row split — replaces the slice-count side of
  * slicing._slice_rows (slicing.py:128-177): per-row slice counts row_cnt[rows],
@@ -118,13 +120,17 @@ int oz_tile_counts(const int32_t* row_cnt, int64_t rows, int32_t* tile_cnt, void
  *   finished tiles per band; the copy stream waits with cuStreamWaitValue32), so
  *   the transfer overlaps the rest of the GEMM; without one, C is copied on
  *   `stream` after the kernel.  Call the copy stream's synchronisation before
- *   reading C_host.  NULL C_host: no copy. */
+ *   reading C_host.  NULL C_host: no copy.
+ *   s_dev (nullable): device int32 {s_A, s_B} written by oz_split_fused; the
+ *   kernel then uses min(sx, s_A) x min(sy, s_B) slice pairs, with sx / sy the
+ *   caps (planes allocated, or max_slices), so no host synchronisation is needed
+ *   between the split and the GEMM. */
 int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64_t ld_b, int planes_a,
                  int planes_b, const int32_t* expo_a, const int32_t* expo_b, const int32_t* tile_cnt_a,
                  const int32_t* tile_cnt_b, int64_t m, int64_t n, int64_t kb, int sx, int sy, int type2,
                  int order, int pair_cutoff, int emu, int accumulate, double* C, int64_t ldc, uint32_t* flags,
                  void* workspace, int64_t workspace_bytes, int pace_slack, double* C_host, int64_t ldc_host,
-                 void* copy_stream, void* stream);
+                 void* copy_stream, const int32_t* s_dev, void* stream);
 
 /* Bytes of device workspace oz_pair_gemm needs for these sizes (0 if there is
  * nothing to compute). */

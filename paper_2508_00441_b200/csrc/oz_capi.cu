@@ -294,7 +294,7 @@ int oz_split_fused(const double* X, int64_t rows, int64_t kb, int64_t ldx, int t
 }
 
 int oz_split_pad(void* coeff, int64_t ld_coeff, int64_t rows, int type2, int s, int32_t* expo,
-                 const int32_t* row_cnt, void* stream) {
+                 const int32_t* row_cnt, const int32_t* s_dev, void* stream) {
   LpFormat f;
   uint32_t idf;
   if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
@@ -303,7 +303,7 @@ int oz_split_pad(void* coeff, int64_t ld_coeff, int64_t rows, int type2, int s, 
   if (!coeff || !expo || !row_cnt) return OZ_EINVAL;
   const unsigned blocks = (unsigned)((rows + 7) / 8);
   oz::pad_planes_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<uint8_t*>(coeff), ld_coeff * f.bytes,
-                                                                   rows, s, expo, row_cnt);
+                                                                   rows, s, expo, row_cnt, s_dev);
   return launch_status();
 }
 
@@ -349,7 +349,7 @@ int oz_split_rows(const double* X, int64_t rows, int64_t kb, int64_t ldx, int ty
                           flags, stream);
   cudaFreeAsync(s_scratch, (cudaStream_t)stream);
   if (rc) return rc;
-  return oz_split_pad(coeff, ld_coeff, rows, type2, planes, expo, row_cnt, stream);
+  return oz_split_pad(coeff, ld_coeff, rows, type2, planes, expo, row_cnt, nullptr, stream);
 }
 
 int oz_transpose(const double* src, int64_t rows, int64_t cols, int64_t ld_src, double* dst, int64_t ld_dst,
@@ -374,7 +374,7 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
                  const int32_t* tile_cnt_b, int64_t m, int64_t n, int64_t kb, int sx, int sy, int type2,
                  int order, int pair_cutoff, int emu, int accumulate, double* C, int64_t ldc, uint32_t* flags,
                  void* workspace, int64_t workspace_bytes, int pace_slack, double* C_host, int64_t ldc_host,
-                 void* copy_stream, void* stream) {
+                 void* copy_stream, const int32_t* s_dev, void* stream) {
   LpFormat f;
   uint32_t idf;
   if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
@@ -400,7 +400,7 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   P.expo_a = expo_a; P.expo_b = expo_b; P.tile_cnt_a = tile_cnt_a; P.tile_cnt_b = tile_cnt_b;
   P.C = C; P.ldc = ldc; P.m = (int)m; P.n = (int)n; P.kb = (int)kb; P.sx = sx; P.sy = sy;
   P.order = order; P.cutoff = pair_cutoff; P.accumulate = accumulate;
-  P.elem_bytes = f.bytes; P.fmt = idf; P.flags = flags;
+  P.elem_bytes = f.bytes; P.fmt = idf; P.flags = flags; P.s_dev = s_dev;
   const PairPlan pl = plan_pair(m, n, sx, sy, pair_cutoff, emu);
   const int cta = pl.cta, tn = pl.tn;
   if (!workspace || (size_t)workspace_bytes < pl.eb_bytes) return OZ_EINVAL;  // see oz_pair_gemm_workspace
@@ -428,7 +428,7 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   P.ebsh = eb_ws;
   P.ebmm = eb_ws + (size_t)sy * P.n_pad;
   oz::prep_eb_kernel<<<dim3((unsigned)P.tiles_n, (unsigned)sy), tn, 0, st>>>(expo_b, (int)n, tn, P.n_pad, P.tiles_n,
-                                                                         eb_ws, eb_ws + (size_t)sy * P.n_pad);
+                                                                         eb_ws, eb_ws + (size_t)sy * P.n_pad, s_dev);
   // Pacing needs an identical pair sequence in every tile (no skipping) and
   // scratch counters (one per tile-wave and pair) after the exponents and the
   // band counters.
@@ -442,20 +442,23 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
     P.pairs_per_tile = pl.pairs;
   }
   // Overlapped device->host copy of C (optional): band counters zeroed on the
-  // copy stream, the kernel waits for that, and per row band the copy stream
-  // waits (cuStreamWaitValue32) for all of the band's tiles, then copies it.
+  // compute stream, the copy stream joins after that memset, and per row band
+  // it waits (cuStreamWaitValue32) for all of the band's tiles, then copies it.
   P.band_done = nullptr;
   cudaStream_t cst = (cudaStream_t)copy_stream;
   StreamWaitFn wait_fn = C_host ? get_wait_value() : nullptr;
   const bool overlap = C_host && cst && wait_fn && ldc_host >= n &&
                        (size_t)workspace_bytes >= pl.eb_bytes + pl.band_bytes;
   if (overlap) {
+    // Zero the counters on the compute stream (ordered after whatever used this
+    // workspace memory before), then let the copy stream start waiting only
+    // after that memset — not after the kernel.
     P.band_done = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(workspace) + pl.eb_bytes);
-    cudaMemsetAsync(P.band_done, 0, pl.band_bytes, cst);
+    cudaMemsetAsync(P.band_done, 0, pl.band_bytes, st);
     cudaEvent_t ev;
     cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    cudaEventRecord(ev, cst);
-    cudaStreamWaitEvent(st, ev, 0);
+    cudaEventRecord(ev, st);
+    cudaStreamWaitEvent(cst, ev, 0);
     cudaEventDestroy(ev);
   }
   if (cta == 1)

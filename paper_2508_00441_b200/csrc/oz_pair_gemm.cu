@@ -81,7 +81,8 @@ struct PairParams {
   double* C;
   int64_t ldc;
   int m, n, kb;
-  int sx, sy;                // slice counts after max_slices
+  int sx, sy;                // slice counts after max_slices (caps when s_dev != nullptr)
+  const int32_t* s_dev;      // nullable: device {s_A, s_B} of the split (counts = min(caps, these))
   int order;                 // 0 = smallest-first, 1 = largest-first
   int cutoff;                // keep pairs with p+q <= cutoff  (< 0: keep all)
   int accumulate;            // 0: C = Cb (first block), 1: C = C + Cb
@@ -271,9 +272,9 @@ OZ_DEVICE uint64_t make_term(uint32_t g, int e1, bool& bad) {
 
 // Pair limits for this CTA's 128-row slab (row128) and the tile's kN columns.
 template <int kN>
-OZ_DEVICE void tile_limits(const PairParams& P, int row128, int tn, int& lp, int& lq) {
-  lp = P.sx;
-  lq = P.sy;
+OZ_DEVICE void tile_limits(const PairParams& P, int sx, int sy, int row128, int tn, int& lp, int& lq) {
+  lp = sx;
+  lq = sy;
   if (P.tile_cnt_a) {
     lp = row128 * kPM < P.m ? min(lp, __ldg(P.tile_cnt_a + row128)) : 0;
     int cq = 0;
@@ -287,11 +288,11 @@ OZ_DEVICE void tile_limits(const PairParams& P, int row128, int tn, int& lp, int
 // halves walk the same pairs (the wider A limit); a half whose rows have an
 // all-zero slice p simply adds nothing for it.
 template <int kCta, int kN>
-OZ_DEVICE void unit_limits(const PairParams& P, int tm, int tn, int& lp_walk, int& lq) {
-  tile_limits<kN>(P, tm * kCta, tn, lp_walk, lq);
+OZ_DEVICE void unit_limits(const PairParams& P, int sx, int sy, int tm, int tn, int& lp_walk, int& lq) {
+  tile_limits<kN>(P, sx, sy, tm * kCta, tn, lp_walk, lq);
   if constexpr (kCta == 2) {
     int lp1, lq1;
-    tile_limits<kN>(P, tm * kCta + 1, tn, lp1, lq1);
+    tile_limits<kN>(P, sx, sy, tm * kCta + 1, tn, lp1, lq1);
     lp_walk = max(lp_walk, lp1);
   }
 }
@@ -452,8 +453,9 @@ OZ_DEVICE void store_row(const PairParams& P, int row, int col0, const Acc* cb, 
 // CTA of kN threads per (tile, q).  Read through L1 by the epilogue, so no smem
 // is spent on exponents and any slice count works.
 __global__ void prep_eb_kernel(const int32_t* __restrict__ expo_b, int n, int kn, int n_pad, int tiles_n,
-                               int32_t* __restrict__ ebsh, int32_t* __restrict__ ebmm) {
+                               int32_t* __restrict__ ebsh, int32_t* __restrict__ ebmm, const int32_t* s_dev) {
   const int tile = blockIdx.x, q = blockIdx.y, c = threadIdx.x, gc = tile * kn + c;
+  if (s_dev && q >= s_dev[1]) return;  // plane beyond the split's s: never read
   const int e = gc < n ? expo_b[(int64_t)q * n + gc] : 0;
   ebsh[(int64_t)q * n_pad + gc] = e * (1 << 20);
   __shared__ int lo[32], hi[32];
@@ -490,6 +492,16 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const uint32_t crank = kCta == 2 ? cluster_rank() : 0;  // rank in the CTA pair
   const bool leader = crank == 0;
   const int num_tiles = P.tiles_m * P.tiles_n;
+  // Slice counts: host values, or caps on the split's device-side counts (no
+  // host round trip between the split and this kernel).
+  int sx = P.sx, sy = P.sy, pairs_per_tile = P.pairs_per_tile;
+  if (P.s_dev) {
+    sx = min(sx, __ldg(P.s_dev));
+    sy = min(sy, __ldg(P.s_dev + 1));
+    pairs_per_tile = 0;
+    for (int p = 0; p < sx; ++p)
+      for (int q = 0; q < sy; ++q) pairs_per_tile += (P.cutoff < 0 || p + q <= P.cutoff) ? 1 : 0;
+  }
   const int unit = blockIdx.x / kCta, num_units = gridDim.x / kCta;  // tile-processing unit (CTA or pair)
   constexpr int kb_elems = 128 / kElemBytes;
   const int num_kb = (P.kb + kb_elems - 1) / kb_elems;
@@ -523,7 +535,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         for (int tile = unit; tile < num_tiles; tile += num_units) {
           int tm, tn, lp, lq;
           tile_coords(tile, P.tiles_m, P.tiles_n, P.group, tm, tn);
-          unit_limits<kCta, kN>(P, tm, tn, lp, lq);
+          unit_limits<kCta, kN>(P, sx, sy, tm, tn, lp, lq);
           const int wave = tile / num_units;
           const int arow = (tm * kCta + (int)crank) * kPM;
           const int brow = tn * kN + (int)crank * Cfg::kBRows;
@@ -535,9 +547,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
               // Wait until every CTA of the wave `pace_slack` steps back has issued its loads.
               // Scheduling only: if that takes implausibly long (CTAs not co-resident),
               // stop pacing instead of risking a deadlock.
-              const int g = wave * P.pairs_per_tile + t - P.pace_slack;
+              const int g = wave * pairs_per_tile + t - P.pace_slack;
               if (g >= 0) {
-                const int gw = g / P.pairs_per_tile;
+                const int gw = g / pairs_per_tile;
                 const uint32_t need = (uint32_t)(kCta * min(num_units, num_tiles - gw * num_units));
                 const long long t0 = clock64();
                 while (ld_relaxed_gpu(P.step_ctr + g) < need) {
@@ -566,7 +578,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 tma_load_3d_pair(s.b[st], &map_b, &s.full[st], kbi * kb_elems, brow, q, P.hint_b);
               }
             }
-            if (P.step_ctr) red_relaxed_gpu_add(P.step_ctr + wave * P.pairs_per_tile + t, 1u);
+            if (P.step_ctr) red_relaxed_gpu_add(P.step_ctr + wave * pairs_per_tile + t, 1u);
           }
         }
       }
@@ -577,7 +589,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       for (int tile = unit; tile < num_tiles; tile += num_units) {
         int tm, tn, lp, lq;
         tile_coords(tile, P.tiles_m, P.tiles_n, P.group, tm, tn);
-        unit_limits<kCta, kN>(P, tm, tn, lp, lq);
+        unit_limits<kCta, kN>(P, sx, sy, tm, tn, lp, lq);
         PairIter pi;
         for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
           const uint32_t buf = acc_it % kAccBufs;
@@ -619,9 +631,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
       int tm, tn, lp, lq;
       tile_coords(tile, P.tiles_m, P.tiles_n, P.group, tm, tn);
       const int row128 = tm * kCta + (int)crank;
-      tile_limits<kN>(P, row128, tn, lp, lq);
+      tile_limits<kN>(P, sx, sy, row128, tn, lp, lq);
       int lp_walk;  // pairs the MMA issuer walks (unit_limits)
-      unit_limits<kCta, kN>(P, tm, tn, lp_walk, lq);
+      unit_limits<kCta, kN>(P, sx, sy, tm, tn, lp_walk, lq);
       const int row = row128 * kPM + quad * 32 + lane;
       // Cb is kept as raw FP64 bit patterns; in emulated mode no double-typed
       // value may exist at all, or nvcc turns bit tricks into FP64 instructions.
@@ -702,8 +714,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
       // C = Cb (first block) or C = C + Cb (ozgemm.py:204-207).  The TMEM reads
       // are warp-collective (.sync.aligned): issue them outside the row guard.
+      const bool store = !(P.debug & 8);  // diagnostics: bit 3 skips the C stores
       if constexpr (kRegCols > 0)
-        if (row < P.m) store_row<kEmu>(P, row, tn * kN + half * 64, cb, 64, flags);
+        if (row < P.m && store) store_row<kEmu>(P, row, tn * kN + half * 64, cb, 64, flags);
       if constexpr (kTmHalf > 0) {
 #pragma unroll(kEmu ? 1 : kTmHalf / 16)
         for (int ch = 0; ch < kTmHalf / 16; ++ch) {
@@ -715,7 +728,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           for (int j = 0; j < 16; ++j) {
             c16[j] = (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
           }
-          if (row < P.m) store_row<kEmu>(P, row, tn * kN + kRegCols + half * kTmHalf + ch * 16, c16, 16, flags);
+          if (row < P.m && store) store_row<kEmu>(P, row, tn * kN + kRegCols + half * kTmHalf + ch * 16, c16, 16, flags);
         }
       }
       // Publish "this tile of C is final" per row band, so a copy stream waiting

@@ -350,10 +350,12 @@ __global__ void __launch_bounds__(kThreads, kThreads <= 256 ? 2 : 1) split_fused
 
 // Zero slices for rows exhausted before the global s (slicing.py:149-152):
 // planes [row_cnt[row], s) of each row and their exponents.  One warp per row.
-__global__ void pad_planes_kernel(uint8_t* __restrict__ coeff, int64_t row_bytes, int64_t rows, int s,
-                                  int32_t* __restrict__ expo, const int32_t* __restrict__ row_cnt) {
+__global__ void pad_planes_kernel(uint8_t* __restrict__ coeff, int64_t row_bytes, int64_t rows, int s_arg,
+                                  int32_t* __restrict__ expo, const int32_t* __restrict__ row_cnt,
+                                  const int32_t* __restrict__ s_dev) {
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (row >= rows) return;
+  const int s = s_dev ? min(*s_dev, s_arg) : s_arg;  // s_arg caps (planes allocated)
   const int lane = threadIdx.x & 31;
   const int cnt = row_cnt[row];
   for (int p = cnt; p < s; ++p) {

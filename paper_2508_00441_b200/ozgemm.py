@@ -30,7 +30,8 @@ import numpy as np
 from . import _lib
 from .errors import DimensionError, SlicingInfeasible
 from .formats import FormatSpec
-from .slicing import compute_params, predict_gemm_count, predict_slice_count, split_many_device, transpose_device
+from .slicing import (compute_params, predict_gemm_count, predict_slice_count, split_deferred, split_many_device,
+                      transpose_device)
 
 __all__ = [
     "DimensionError", "GemmConfig", "BlockStats", "OzStats", "OzResult", "transpose", "oz_gemm",
@@ -197,12 +198,19 @@ def _panel_plan(m: int, n: int, kb: int, eb: int, torch) -> tuple[int, int]:
     return mp, np_
 
 
-def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_out=None):
+def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_out=None, deferred: bool = True):
     """C = A @ B for CUDA float64 tensors; returns (C, OzStats).  No host copies
     of operands or result (the timed hot path of bench.py) unless ``host_out`` (a
     pinned CPU float64 tensor) is given: then C is also copied there, band by band
     on a side stream while the last block's GEMM still runs (single-panel runs;
-    otherwise after it)."""
+    otherwise after it).
+
+    ``deferred`` (default): no host synchronisation until the end — the splits
+    leave s on the device and the pair GEMM reads it there; the s values, the
+    split flags (checked A before B, block by block, as the reference raises)
+    and the GEMM flags are read once at the end.  If a split ran out of
+    one-pass planes (rare, very wide exponent ranges) the call is redone with
+    the exact two-pass split (``deferred=False``)."""
     torch = _lib.require_cuda()
     if A.ndim != 2 or B.ndim != 2 or A.shape[1] != B.shape[0]:
         raise DimensionError(f"cannot multiply shapes {tuple(A.shape)} and {tuple(B.shape)}")
@@ -217,10 +225,10 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
     C = out if out is not None else torch.empty((m, n), dtype=torch.float64, device=A.device)
     sp = _lib.stream_ptr(torch)
     flags = torch.zeros(1, dtype=torch.int32, device=A.device)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timing else None
-    t_slice = t_gemm = 0.0
+    evs = []  # (split start, split end, gemm end) per pass
     eb = _lib.ELEM_BYTES.get(cfg.type2.name, 1)
     mp, np_ = m, n
+    blocks = []  # per block: (lo, hi, kb, [A sf tensors], [B sf tensors], s_a, s_b)
     for bi, (lo, hi) in enumerate(_blocks(k, cfg.k_block)):
         kb = hi - lo
         params = compute_params(53, cfg.type2.mant_bits, cfg.type3.mant_bits, kb)
@@ -230,36 +238,68 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
         _check_accumulator(params, kb)
         mp, np_ = _panel_plan(m, n, kb, eb, torch) if m and n else (max(m, 1), max(n, 1))
         s_a = s_b = 0
+        sfa, sfb = [], []
         for j0 in range(0, max(n, 1), np_):
             j1 = min(n, j0 + np_)
             for i0 in range(0, max(m, 1), mp):
                 i1 = min(m, i0 + mp)
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timing else None
                 if timing:
                     ev[0].record()
-                # Row panel of A, column panel of B (columns as K-major rows).  The
-                # reference slices A before B; with panels, B's panel is re-sliced
-                # per A panel only when it changes (j0 loop outside).
-                if i0 == 0:
-                    Bt = transpose_device(B[lo:hi, j0:j1])
-                    (sa, sb), _ = split_many_device([A[i0:i1, lo:hi], Bt], cfg.type2, params, emu,
-                                                    flags_out=flags)
+                # Row panel of A, column panel of B (columns as K-major rows); B's
+                # panel is sliced once per column panel (j0 loop outside).
+                if deferred:
+                    sa = split_deferred(A[i0:i1, lo:hi], cfg.type2, params, emu)
+                    sfa.append(sa.sf)
+                    if i0 == 0:
+                        Bt = transpose_device(B[lo:hi, j0:j1])
+                        sb = split_deferred(Bt, cfg.type2, params, emu)
+                        sfb.append(sb.sf)
+                    s_dev = torch.cat([sa.sf[:1], sb.sf[:1]])
                 else:
-                    (sa,), _ = split_many_device([A[i0:i1, lo:hi]], cfg.type2, params, emu, flags_out=flags)
+                    if i0 == 0:
+                        Bt = transpose_device(B[lo:hi, j0:j1])
+                        (sa, sb), _ = split_many_device([A[i0:i1, lo:hi], Bt], cfg.type2, params, emu,
+                                                        flags_out=flags)
+                    else:
+                        (sa,), _ = split_many_device([A[i0:i1, lo:hi]], cfg.type2, params, emu,
+                                                     flags_out=flags)
+                    s_a, s_b = max(s_a, sa.s), max(s_b, sb.s)
+                    s_dev = None
                 if timing:
                     ev[1].record()
-                s_a, s_b = max(s_a, sa.s), max(s_b, sb.s)
                 last = hi == k and j1 == n and i1 == m
                 host = None
                 if host_out is not None and last and mp == m and np_ == n:
                     host = (host_out, _copy_stream(torch).cuda_stream)
                 _pair_pass(torch, cfg, sa, sb, i1 - i0, j1 - j0, kb, order, cutoff, emu, bi, C, i0, j0, n,
-                           flags, sp, host)
+                           flags, sp, host, s_dev)
                 if timing:
                     ev[2].record()
-                    ev[2].synchronize()
-                    t_slice += ev[0].elapsed_time(ev[1]) / 1e3
-                    t_gemm += ev[1].elapsed_time(ev[2]) / 1e3
+                    evs.append(ev)
             del Bt, sb
+        blocks.append((lo, hi, kb, sfa, sfb, s_a, s_b))
+    if host_out is not None:
+        if mp == m and np_ == n and m and n:
+            _copy_stream(torch).synchronize()
+        else:  # panelled: plain copy after the last panel
+            host_out.copy_(C)
+    # The one synchronisation: split counts / flags (deferred mode) + GEMM flags.
+    words = [flags] + [t for b in blocks for t in b[3] + b[4]]
+    host = torch.cat(words).cpu().tolist()
+    gemm_flags, pos = host[0] & 0xFFFFFFFF, 1
+    split_words = []
+    for lo, hi, kb, sfa, sfb, s_a, s_b in blocks:
+        fa, fb = [], []
+        for _ in sfa:
+            s_a = max(s_a, host[pos])
+            fa.append(host[pos + 1] & 0xFFFFFFFF)
+            pos += 2
+        for _ in sfb:
+            s_b = max(s_b, host[pos])
+            fb.append(host[pos + 1] & 0xFFFFFFFF)
+            pos += 2
+        split_words.append((fa, fb))
         sx = min(s_a, cfg.max_slices or s_a)
         sy = min(s_b, cfg.max_slices or s_b)
         kept = len(pair_order(sx, sy, cfg.accumulation_order, cfg.pair_cutoff)) \
@@ -269,14 +309,15 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
         stats.gemm_count += kept
         stats.gemm_ops += 2 * m * n * kb * kept
         stats.accum_ops += 2 * m * n * kept + m * n
-    if host_out is not None:
-        if mp == m and np_ == n and m and n:
-            _copy_stream(torch).synchronize()
-        else:  # panelled: plain copy after the last panel
-            host_out.copy_(C)
-    f = int(flags.item()) & 0xFFFFFFFF
-    _lib.raise_for_flags(f, "pair gemm")
-    stats.t_slice, stats.t_gemm = t_slice, t_gemm
+    if any(f & _lib.FLAG_PLANE_CAP for fa, fb in split_words for f in fa + fb):
+        return oz_gemm_device(A, B, cfg, out=C, timing=timing, host_out=host_out, deferred=False)
+    for fa, fb in split_words:  # reference order: block by block, A before B
+        for f in fa + fb:
+            _lib.raise_for_flags(f, "split")
+    _lib.raise_for_flags(gemm_flags, "pair gemm")
+    if timing:
+        stats.t_slice = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3
+        stats.t_gemm = sum(e[1].elapsed_time(e[2]) for e in evs) / 1e3
     return C, stats
 
 
@@ -291,7 +332,8 @@ def _copy_stream(torch):
     return _COPY_STREAMS[d]
 
 
-def _pair_pass(torch, cfg, sa, sb, m, n, kb, order, cutoff, emu, bi, C, i0, j0, ldc, flags, sp, host=None):
+def _pair_pass(torch, cfg, sa, sb, m, n, kb, order, cutoff, emu, bi, C, i0, j0, ldc, flags, sp, host=None,
+               s_dev=None):
     """One fused pair-GEMM launch for the C panel [i0:i0+m, j0:j0+n]."""
     sx = min(sa.s, cfg.max_slices or sa.s)
     sy = min(sb.s, cfg.max_slices or sb.s)
@@ -303,6 +345,12 @@ def _pair_pass(torch, cfg, sa, sb, m, n, kb, order, cutoff, emu, bi, C, i0, j0, 
         _lib.call("oz_tile_counts", sb.row_cnt.data_ptr(), n, tcb.data_ptr(), sp)
     ws_bytes = _lib.load().oz_pair_gemm_workspace(m, n, sx, sy, cutoff) if m and n and sx and sy else 0
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=C.device)
+    if host:
+        # The copy stream waits on the band counters inside ws and reads C: keep
+        # both out of the caching allocator's reuse until that stream is done.
+        cs = _copy_stream(torch)
+        ws.record_stream(cs)
+        C.record_stream(cs)
     Cp = C[i0:, j0:] if (i0 or j0) else C
     _lib.call("oz_pair_gemm",
               sa.planes.data_ptr() if sa.s else None, sb.planes.data_ptr() if sb.s else None,
@@ -314,7 +362,7 @@ def _pair_pass(torch, cfg, sa, sb, m, n, kb, order, cutoff, emu, bi, C, i0, j0, 
               int(bi > 0), Cp.data_ptr(), ldc, flags.data_ptr(),
               ws.data_ptr(), ws_bytes, PACE_SLACK,
               host[0].data_ptr() if host else None, host[0].shape[1] if host else 0,
-              host[1] if host else None, sp)
+              host[1] if host else None, s_dev.data_ptr() if s_dev is not None else None, sp)
 
 
 def oz_gemm(A, B, cfg: GemmConfig) -> OzResult:

@@ -33,7 +33,7 @@ from .formats import FormatSpec, decode_codes
 __all__ = [
     "SlicingInfeasible", "SlicingParams", "SliceSet", "DeviceSlices", "compute_params",
     "predict_slice_count", "predict_gemm_count", "slice_vector", "slice_matrix", "split_rows_device",
-    "split_many_device",
+    "split_many_device", "split_deferred",
 ]
 
 
@@ -102,7 +102,9 @@ class SliceSet:
 class DeviceSlices:
     """Slices resident in HBM, laid out for TMA: ``planes`` uint8
     ``[s, rows, ld * elem_bytes]`` (K-major codes, zero padded), ``expo`` int32
-    ``[s, rows]``, ``row_cnt`` int32 ``[rows]`` (per-row slice counts)."""
+    ``[s, rows]``, ``row_cnt`` int32 ``[rows]`` (per-row slice counts).
+    Deferred splits (no host sync) hold ``cap`` planes, ``s`` = cap, and the
+    true s and the flag word in the device tensor ``sf`` = [s, flags]."""
 
     planes: object
     expo: object
@@ -112,6 +114,7 @@ class DeviceSlices:
     kb: int
     ld: int
     fmt: FormatSpec
+    sf: object = None
 
     def codes(self):
         """Codes as a [s, rows, kb] uint8/uint16 torch tensor view."""
@@ -221,10 +224,38 @@ def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, str
             planes, expo = planes[:s_max], expo[:s_max]
             if s_max > 0 and rows > 0:
                 _lib.call("oz_split_pad", planes.data_ptr(), ld, rows, code, s_max, expo.data_ptr(),
-                          row_cnt.data_ptr(), sp)
+                          row_cnt.data_ptr(), None, sp)
         all_flags |= flags
         out.append(DeviceSlices(planes, expo, row_cnt[:rows], s_max, rows, kb, ld, fmt))
     return out, all_flags
+
+
+def split_deferred(X, fmt: FormatSpec, params: SlicingParams, emu: bool, stream=None) -> DeviceSlices:
+    """One-pass split without a host synchronisation: the fused split and the
+    zero padding (which reads s on the device) are only enqueued.  The result
+    holds ``cap`` planes; the pair GEMM takes the true s from ``sf`` on the
+    device.  The caller reads ``sf`` later and must redo the work with
+    ``split_many_device`` if its flags carry ``FLAG_PLANE_CAP``."""
+    torch = _lib.require_cuda()
+    code = _fmt_code(fmt)
+    sp = stream if stream is not None else _lib.stream_ptr(torch)
+    eb = _lib.ELEM_BYTES[fmt.name]
+    rows, kb = X.shape
+    if X.dtype != torch.float64 or (X.stride(1) != 1 and kb > 1):
+        raise ValueError("split expects a float64 view with unit column stride")
+    ldx = X.stride(0) if rows > 1 else kb
+    ld = -(-kb // (16 // eb)) * (16 // eb)
+    cap = _plane_cap(rows, ld * eb, predict_slice_count(params) or 1)
+    sf = torch.zeros(2, dtype=torch.int32, device=X.device)
+    row_cnt = torch.empty(max(rows, 1), dtype=torch.int32, device=X.device)
+    planes = torch.empty((cap, rows, ld * eb), dtype=torch.uint8, device=X.device)
+    expo = torch.empty((cap, rows), dtype=torch.int32, device=X.device)
+    if rows > 0:
+        _lib.call("oz_split_fused", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu), cap,
+                  planes.data_ptr(), ld, expo.data_ptr(), row_cnt.data_ptr(), sf.data_ptr(), sf.data_ptr() + 4, sp)
+        _lib.call("oz_split_pad", planes.data_ptr(), ld, rows, code, cap, expo.data_ptr(), row_cnt.data_ptr(),
+                  sf.data_ptr(), sp)
+    return DeviceSlices(planes, expo, row_cnt[:rows], cap, rows, kb, ld, fmt, sf)
 
 
 def _to_device_f64(M):

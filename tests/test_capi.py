@@ -56,7 +56,7 @@ def test_argument_errors_return_status_without_gpu(lib):
     assert lib.oz_transpose(None, -1, 2, 2, None, 2, None) == 1
     assert lib.oz_split_count(None, 4, 8, 8, 9, 49, 0, None, None, None, None) == 2  # bad type2
     assert lib.oz_pair_gemm(None, None, 16, 16, 1, 1, None, None, None, None, 4, 4, 16, 2, 1, 0, 0, -1, 0, 0,
-                            None, 4, None, None, 0, 0, None, 0, None, None) == 1
+                            None, 4, None, None, 0, 0, None, 0, None, None, None) == 1
 
 
 def _sass_of(lib_path, kernel_substr):
