@@ -250,10 +250,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Test hook: OZ_BENCH_ONE_GPU=1 puts every rank on cuda:0 with the gloo
+    # backend, to exercise the multi-rank path on a single-GPU box.
+    one_gpu = os.environ.get("OZ_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     n = args.n
     cfg = oz.GemmConfig(oz.get_format(args.type2), oz.get_format(args.type3), k_block=args.kblock,
                         fp64_emulation=args.emu, max_slices=args.max_slices, pair_cutoff=args.pair_cutoff,
