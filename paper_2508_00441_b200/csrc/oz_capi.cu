@@ -414,6 +414,16 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
     P.hint_b = hints[hb ? (atoi(hb) % 3 + 3) % 3 : 0];
   }
   if (const char* e = getenv("OZ_GROUP")) P.group = atoi(e) > 0 ? atoi(e) : 8;
+  // Diagnostics: OZ_TRACE=<device address hex>:<entries> (tools/k3_trace.py).
+  P.trace = nullptr; P.trace_cap = 0;
+  if (const char* e = getenv("OZ_TRACE")) {
+    unsigned long long addr = 0;
+    int cap = 0;
+    if (sscanf(e, "%llx:%d", &addr, &cap) == 2) {
+      P.trace = reinterpret_cast<unsigned long long*>(addr);
+      P.trace_cap = cap;
+    }
+  }
   CUtensorMap ma, mb;
   int rc = make_plane_map(&ma, a_planes, f.bytes, kb, m, planes_a, ld_a, oz::kPM);
   if (rc) return rc;

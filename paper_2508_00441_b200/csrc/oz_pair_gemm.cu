@@ -99,6 +99,8 @@ struct PairParams {
   int group;                 // raster band height in row-tiles
   uint64_t hint_a, hint_b;   // L2 cache policies of the operand loads
   uint32_t* band_done;       // [tiles_m / group] finished-tile counters (nullable)
+  unsigned long long* trace; // diagnostics (nullable): per-pair timestamps of unit 0
+  int trace_cap;             // entries (pairs) the trace holds
   // Diagnostics only (OZ_DEBUG_MODE): bit 0 = epilogue skips TMEM loads/math,
   // bit 1 = producer stops loading after the first ring fill (stale operands),
   // bit 2 = MMA issuer ignores the stage barriers (pure issue rate).
@@ -593,12 +595,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
         PairIter pi;
         for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
           const uint32_t buf = acc_it % kAccBufs;
+          const bool tr = P.trace && unit == 0 && acc_it < (uint32_t)P.trace_cap;
+          long long full_wait = 0;
+          if (tr && lane == 0) P.trace[acc_it * 8 + 0] = clock64();
           if (acc_it >= (uint32_t)kAccBufs) mbar_wait(&s.acc_empty[buf], ((acc_it / kAccBufs) - 1) & 1);
+          if (tr && lane == 0) P.trace[acc_it * 8 + 1] = clock64();
           tc_fence_after();
           const uint32_t d_tmem = tmem + buf * kN;
           for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
             const uint32_t st = it % kStages;
+            const long long tw0 = tr ? clock64() : 0;
             if (!(P.debug & 4)) mbar_wait(&s.full[st], (it / kStages) & 1);  // bit 2: diagnostics, no waits
+            if (tr) full_wait += clock64() - tw0;
             tc_fence_after();
             if (elect_one()) {
               const uint64_t ad = smem_desc_sw128(s.a[st]), bd = smem_desc_sw128(s.b[st]);
@@ -612,6 +620,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
             __syncwarp();
           }
           if (elect_one()) mma_commit_g<kCta>(&s.acc_full[buf]);
+          if (tr && lane == 0) {
+            P.trace[acc_it * 8 + 2] = clock64();
+            P.trace[acc_it * 8 + 6] = (unsigned long long)full_wait;
+          }
           __syncwarp();
         }
       }
@@ -654,7 +666,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
       for (pi.init(lp_walk, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
         const int p = pi.p, q = pi.q();
         const uint32_t buf = acc_it % kAccBufs;
+        const bool tr = P.trace && unit == 0 && crank == 0 && warp == 4 && lane == 0 && acc_it < (uint32_t)P.trace_cap;
+        if (tr) P.trace[acc_it * 8 + 3] = clock64();
         mbar_wait(&s.acc_full[buf], (acc_it / kAccBufs) & 1);
+        if (tr) P.trace[acc_it * 8 + 4] = clock64();
         tc_fence_after();
         // p >= lp: this CTA's rows have an all-zero A slice p (the partner needs it):
         // the term is +0, nothing to add.
@@ -679,6 +694,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
               if (ch + 1 < 4) tmem_ld_wait_regs(g[(ch + 1) & 1]);
             }
           }
+          if (tr) P.trace[acc_it * 8 + 7] = clock64();
           if constexpr (kTmHalf > 0) {
 #pragma unroll(kEmu ? 1 : kTmHalf / 16)
             for (int ch = 0; ch < kTmHalf / 16; ++ch) {
@@ -706,6 +722,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
+        if (tr) P.trace[acc_it * 8 + 5] = clock64();
         if (lane == 0) {
           if constexpr (kCta == 1) mbar_arrive(&s.acc_empty[buf]);
           else mbar_arrive_cluster(&s.acc_empty[buf], 0);
