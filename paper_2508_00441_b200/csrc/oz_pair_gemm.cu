@@ -680,6 +680,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
           const int2 mm = __ldg(reinterpret_cast<const int2*>(P.ebmm) + (int64_t)q * P.tiles_n + tn);
           const bool safe = ea + 896 + mm.x + 119 >= 1 && ea + 896 + mm.y + 143 <= 2046;
           const int32_t* ebq = P.ebsh + (int64_t)q * P.n_pad + tn * kN;
+          // Pull this pair's B-exponent lines into L1 now: the loads that use them
+          // come after the first DADD, i.e. in the short window in which the
+          // epilogue's DADDs can drain, where an L2 miss would stall.
+          if (lane < (kRegCols > 0 ? 2 : 0) + (kTmHalf * 4 + 127) / 128) {
+            const int32_t* pf = lane < (kRegCols > 0 ? 2 : 0) ? ebq + half * 64 + lane * 32
+                                                               : ebq + kRegCols + half * kTmHalf;
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(pf));
+          }
           const uint32_t gaddr = tmem + lane_base + buf * kN;
           // Software-pipelined TMEM reads: chunk ch+1 loads while chunk ch is
           // accumulated (the wait names the registers so no use is hoisted above it).
