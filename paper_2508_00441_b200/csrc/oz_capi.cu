@@ -233,7 +233,16 @@ PairPlan plan_pair(int64_t m, int64_t n, int sx, int sy, int pair_cutoff, int em
   // OZ_CTA_GROUP=1|2 and OZ_TILE_N=128|192 override (experiments, tests).
   pl.cta = m > oz::kPM ? 2 : 1;
   if (const char* e = getenv("OZ_CTA_GROUP")) pl.cta = atoi(e) == 1 ? 1 : 2;
-  pl.tn = (pl.cta == 2 && n > 128 && !emu) ? 192 : 128;
+  pl.tn = 128;
+  if (pl.cta == 2 && n > 128 && !emu) {
+    // N = 192 unless tile quantisation favours N = 128: time ~ waves x N / efficiency,
+    // with N = 192 measured ~1.07x more efficient per column (n = 2048: N = 128 is
+    // 36% faster, n = 4096 even, n >= 6144 N = 192 wins; profiles/variant_sweep_r01.txt).
+    const int64_t units = num_sms() / 2, tm = (m + 2 * oz::kPM - 1) / (2 * oz::kPM);
+    const int64_t w192 = (tm * ((n + 191) / 192) + units - 1) / units;
+    const int64_t w128 = (tm * ((n + 127) / 128) + units - 1) / units;
+    pl.tn = (double)w192 * 192.0 <= (double)w128 * 128.0 * 1.07 ? 192 : 128;
+  }
   if (const char* e = getenv("OZ_TILE_N")) pl.tn = (atoi(e) == 192 && pl.cta == 2 && !emu) ? 192 : 128;
   pl.tiles_m = (int)((m + oz::kPM * pl.cta - 1) / (oz::kPM * pl.cta));
   pl.tiles_n = (int)((n + pl.tn - 1) / pl.tn);
