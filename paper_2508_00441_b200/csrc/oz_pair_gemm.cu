@@ -101,9 +101,8 @@ struct PairParams {
   uint32_t* band_done;       // [tiles_m / group] finished-tile counters (nullable)
   unsigned long long* trace; // diagnostics (nullable): per-pair timestamps of unit 0
   int trace_cap;             // entries (pairs) the trace holds
-  // Diagnostics only (OZ_DEBUG_MODE): bit 0 = epilogue skips TMEM loads/math,
-  // bit 1 = producer stops loading after the first ring fill (stale operands),
-  // bit 2 = MMA issuer ignores the stage barriers (pure issue rate).
+  // Diagnostics only (OZ_DEBUG_MODE): bit 0 = epilogue skips the accumulation
+  // (MMA-only timing), bit 3 = no C stores.  Results are wrong with either.
   int debug;
 };
 
@@ -566,10 +565,6 @@ __global__ void __launch_bounds__(kPThreads, 1)
             for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
               const uint32_t st = it % kStages;
               if (it >= (uint32_t)kStages) mbar_wait(&s.empty[st], ((it / kStages) - 1) & 1);
-              if ((P.debug & 2) && it >= (uint32_t)kStages) {  // diagnostics: no memory traffic
-                if (leader) mbar_arrive(&s.full[st]);
-                continue;
-              }
               if constexpr (kCta == 1) {
                 mbar_arrive_expect_tx(&s.full[st], Cfg::kStageBytes);
                 tma_load_3d(s.a[st], &map_a, &s.full[st], kbi * kb_elems, arow, p, P.hint_a);
@@ -605,7 +600,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
             const uint32_t st = it % kStages;
             const long long tw0 = tr ? clock64() : 0;
-            if (!(P.debug & 4)) mbar_wait(&s.full[st], (it / kStages) & 1);  // bit 2: diagnostics, no waits
+            mbar_wait(&s.full[st], (it / kStages) & 1);
             if (tr) full_wait += clock64() - tw0;
             tc_fence_after();
             if (elect_one()) {
