@@ -39,7 +39,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "FP64-equiv TFLOPS, Ozaki-FP8 DGEMM n=8192 vs native DGEMM; max rel error"
 UNIT = "TFLOP/s (FP64-equivalent)"
-KERNELS_PER_BLOCK = 8  # split_count x2, transpose, split_rows x2, tile_counts x2, pair_gemm
+KERNELS_PER_BLOCK = 7  # transpose, split_fused x2, split_pad x2, prep_eb, pair_gemm (per block, per step)
 
 
 def parse():
