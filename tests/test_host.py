@@ -134,3 +134,59 @@ def test_backend_fails_loudly_without_gpu():
     cfg = oz.GemmConfig(oz.get_format("fp8e4m3"), oz.get_format("fp32"))
     with pytest.raises(oz.BackendUnavailable):
         oz.oz_gemm(np.ones((2, 2)), np.ones((2, 2)), cfg)
+
+
+class _FakeCuda:
+    """Just enough of torch.cuda for the panel planner (no GPU)."""
+
+    def __init__(self, total_gib, free_gib):
+        self.total, self.free = total_gib << 30, free_gib << 30
+
+    def current_device(self):
+        return 0
+
+    def get_device_properties(self, d):
+        return type("P", (), {"total_memory": self.total})
+
+    def mem_get_info(self):
+        return self.free, self.total
+
+
+def test_panel_plan_small_problems_unpanelled():
+    from paper_2508_00441_b200 import ozgemm
+
+    ozgemm._TOTAL_MEM.clear()
+    torch = type("T", (), {"cuda": _FakeCuda(178, 170)})
+    for n in (128, 1024, 8192, 16384):
+        assert ozgemm._panel_plan(n, n, n, 1, torch) == (n, n)
+
+
+def test_panel_plan_n65536_one_gpu_fits():
+    """n = 65536 FP8 next to 96 GiB of FP64 operands: panels whose slice buffers fit."""
+    from paper_2508_00441_b200 import ozgemm
+    from paper_2508_00441_b200.slicing import PLANE_CAP, _plane_cap
+
+    ozgemm._TOTAL_MEM.clear()
+    torch = type("T", (), {"cuda": _FakeCuda(178, 178 - 96)})
+    n = 65536
+    mp, np_ = ozgemm._panel_plan(n, n, n, 1, torch)
+    assert mp < n and np_ < n and n % mp == 0 and n % np_ == 0
+    ld = n
+    need = 8 * n * np_ + max(_plane_cap(np_, ld, 15), 24) * np_ * ld + max(_plane_cap(mp, ld, 15), 24) * mp * ld
+    assert need <= (178 - 96 - 6) << 30
+    assert PLANE_CAP >= 24
+
+
+def test_fp64_level_summary_picks_fastest_accurate_variant():
+    import bench
+
+    extras = {"accuracy": {"max_rel_err_ozaki": 8e-12, "max_rel_err_cublas_dgemm": 3e-9},
+              "native_dgemm": {"tflops": 35.0},
+              "variants": {"fp8_pair_cutoff_12": {"tflops": 26.0, "max_rel_err": 8e-12},
+                           "fp8_pair_cutoff_11": {"tflops": 30.0, "max_rel_err": 4e-10},
+                           "fp8_pair_cutoff_10": {"tflops": 36.0, "max_rel_err": 4e-9},
+                           "fp8_emulated_fp64": {"tflops": 6.0, "max_rel_err": 8e-12}}}
+    s = bench.fp64_level_summary(extras)
+    assert s["config"].startswith("pair_cutoff_11") and s["tflops"] == 30.0
+    assert abs(s["vs_native_dgemm"] - 30.0 / 35.0) < 1e-12
+    assert bench.fp64_level_summary({}) is None
