@@ -17,7 +17,8 @@
  *   - return value: OZ_OK or an OZ_E* status (launch-time argument errors).
  *
  * type2 codes (slice storage format, formats.py:85-100):
- *   OZ_FMT_E4M3 = 0 (fp8e4m3), OZ_FMT_E5M2 = 1 (fp8e5m2), OZ_FMT_FP16 = 2, OZ_FMT_BF16 = 3
+ *   OZ_FMT_E4M3 = 0 (fp8e4m3), OZ_FMT_E5M2 = 1 (fp8e5m2), OZ_FMT_FP16 = 2, OZ_FMT_BF16 = 3,
+ *   OZ_FMT_E3M2 = 4 (fp6e3m2), OZ_FMT_E2M3 = 5 (fp6e2m3) — FP6 codes one per byte
  */
 #ifndef OZ_B200_H
 #define OZ_B200_H
@@ -38,7 +39,7 @@ enum {
   OZ_ESLICES = 5       /* reserved (earlier versions: slice-count limit)       */
 };
 
-enum { OZ_FMT_E4M3 = 0, OZ_FMT_E5M2 = 1, OZ_FMT_FP16 = 2, OZ_FMT_BF16 = 3 };
+enum { OZ_FMT_E4M3 = 0, OZ_FMT_E5M2 = 1, OZ_FMT_FP16 = 2, OZ_FMT_BF16 = 3, OZ_FMT_E3M2 = 4, OZ_FMT_E2M3 = 5 };
 
 /* device error-flag bits */
 #define OZ_FLAG_NONFINITE_INPUT (1u << 0)   /* slicing.py:120-121  -> ValueError        */

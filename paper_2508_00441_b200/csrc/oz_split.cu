@@ -25,6 +25,7 @@ struct LpFormat {
   int max_field;    // largest exponent field holding finite values
   int nan_top;      // 1: the all-ones mantissa in max_field is NaN (E4M3)
   int bytes;
+  int shift;        // code position inside its container (FP6 in a byte)
 };
 
 // FP64 bit pattern of a slice value v (a multiple of 2^(c+rho-53), |v| <= 2^c)
@@ -52,7 +53,7 @@ OZ_DEVICE uint32_t encode_coeff(uint64_t vb, int c, const LpFormat& f, uint32_t&
       code = (uint32_t)(sig >> drop);
     }
   }
-  return sign | code;
+  return (sign | code) << f.shift;
 }
 
 // ─────────────────────── K1 fused: one pass, table encode ───────────────────────

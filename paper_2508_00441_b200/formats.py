@@ -16,6 +16,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 __all__ = [
@@ -104,6 +106,10 @@ def _minifloat_table(ebits: int, mbits: int, bias: int) -> np.ndarray:
 
 _E4M3_LUT = _minifloat_table(4, 3, 7)
 _E5M2_LUT = _minifloat_table(5, 2, 15)
+_E3M2_LUT = _minifloat_table(3, 2, 3)[:64]
+_E2M3_LUT = _minifloat_table(2, 3, 1)[:64]
+# Bit position of an FP6 code inside its byte (kept equal to the C library's).
+FP6_SHIFT = int(os.environ.get("OZ_FP6_SHIFT", "0"))
 
 
 def decode_codes(codes: np.ndarray, fmt_name: str) -> np.ndarray:
@@ -112,6 +118,9 @@ def decode_codes(codes: np.ndarray, fmt_name: str) -> np.ndarray:
         return _E4M3_LUT[codes.astype(np.intp)]
     if fmt_name == "fp8e5m2":
         return _E5M2_LUT[codes.astype(np.intp)]
+    if fmt_name in ("fp6e3m2", "fp6e2m3"):
+        lut = _E3M2_LUT if fmt_name == "fp6e3m2" else _E2M3_LUT
+        return lut[(codes.astype(np.intp) >> FP6_SHIFT) & 63]
     if fmt_name == "fp16":
         return codes.astype(np.uint16).view(np.float16).astype(np.float64)
     if fmt_name == "bf16":

@@ -39,13 +39,17 @@ def encode_values(vals: np.ndarray, fmt: FormatSpec) -> np.ndarray:
     """Exact float64 values -> storage codes (uint8 / uint16); raises
     RepresentabilityError for a value the format cannot hold exactly."""
     vals = np.asarray(vals, dtype=np.float64)
-    if fmt.name in ("fp8e4m3", "fp8e5m2"):
+    if fmt.name in ("fp8e4m3", "fp8e5m2", "fp6e3m2", "fp6e2m3"):
         table = decode_codes(np.arange(256, dtype=np.uint8), fmt.name)
         ok = np.isfinite(table)
         if fmt.name == "fp8e4m3":
             ok &= np.arange(256) & 0x7F != 0x7F  # S.1111.111 is NaN
-        else:
+        elif fmt.name == "fp8e5m2":
             ok &= (np.arange(256) >> 2) & 0x1F != 0x1F
+        else:  # FP6: only canonical containers (the code at FP6_SHIFT, other bits 0)
+            from .formats import FP6_SHIFT
+
+            ok &= (np.arange(256) & ~(63 << FP6_SHIFT)) == 0
         codes_ok = np.nonzero(ok)[0]
         vals_ok = table[codes_ok]
         order = np.argsort(vals_ok, kind="stable")

@@ -218,6 +218,8 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
     n = B.shape[1]
     if cfg.k_block > k:
         raise ValueError("k_block exceeds k")
+    if cfg.type2.name in _FP6:
+        deferred = False  # split errors (fp6e2m3: SlicingInfeasible) before the unsupported GEMM
     emu = bool(cfg.fp64_emulation)
     order = 0 if cfg.accumulation_order == "smallest-first" else 1
     cutoff = -1 if cfg.pair_cutoff is None else int(cfg.pair_cutoff)
@@ -257,13 +259,13 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
                         sfb.append(sb.sf)
                     s_dev = torch.cat([sa.sf[:1], sb.sf[:1]])
                 else:
+                    fo = None if cfg.type2.name in _FP6 else flags  # FP6: raise split errors right away
                     if i0 == 0:
                         Bt = transpose_device(B[lo:hi, j0:j1])
                         (sa, sb), _ = split_many_device([A[i0:i1, lo:hi], Bt], cfg.type2, params, emu,
-                                                        flags_out=flags)
+                                                        flags_out=fo)
                     else:
-                        (sa,), _ = split_many_device([A[i0:i1, lo:hi]], cfg.type2, params, emu,
-                                                     flags_out=flags)
+                        (sa,), _ = split_many_device([A[i0:i1, lo:hi]], cfg.type2, params, emu, flags_out=fo)
                     s_a, s_b = max(s_a, sa.s), max(s_b, sb.s)
                     s_dev = None
                 if timing:
@@ -322,6 +324,7 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
 
 
 _COPY_STREAMS = {}
+_FP6 = ("fp6e3m2", "fp6e2m3")
 
 
 def _copy_stream(torch):

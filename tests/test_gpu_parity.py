@@ -218,3 +218,27 @@ def test_host_output_overlapped_copy(cuda, kbk):
     assert not rh.C.is_cuda
     assert np.array_equal(bits(rh.C.numpy()), bits(rd.C.cpu().numpy()))
     assert np.array_equal(bits(rn.C), bits(rd.C.cpu().numpy()))
+
+
+def test_fp6_formats(cuda):
+    """FP6 slices: the split is exact (fp6e3m2 planes bitwise vs the oracle) and
+    fp6e2m3 fails the reference's way (SlicingInfeasible, slicing.py:169-172);
+    fp6e3m2 slice products are not wired to tcgen05 yet (NotImplementedError,
+    tools/fp6_probe.py) — never a silent CPU path."""
+    import oracle
+
+    oz = _oz()
+    rng = np.random.default_rng(66)
+    A = spread_matrix(rng, 40, 96, 0.5)
+    B = spread_matrix(rng, 96, 24, 0.5)
+    f = oz.get_format("fp6e3m2")
+    params = oz.compute_params(53, f.mant_bits, 24, 96)
+    ss = oz.slice_matrix(A, "rows", f, params)
+    coeff, expo, _, s, flags = oracle.split_rows(A, params.rho, False)
+    assert flags == 0 and ss.s == s
+    for p in range(s):
+        assert np.array_equal(bits(ss.coeff[p]), bits(coeff[p]))
+    with pytest.raises(NotImplementedError):
+        oz.oz_gemm(A, B, oz.GemmConfig(f, oz.get_format("fp32")))
+    with pytest.raises(oz.SlicingInfeasible):
+        oz.oz_gemm(A, B, oz.GemmConfig(oz.get_format("fp6e2m3"), oz.get_format("fp32")))
