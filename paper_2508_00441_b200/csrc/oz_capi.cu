@@ -70,17 +70,24 @@ StreamWaitFn get_wait_value() {
   return fn;
 }
 
+// fp6: planes hold packed FP6 groups (16 codes in 12 bytes + 4 zero bytes per 16
+// bytes, written by the split); TMA's 16U6_ALIGN16B type unpacks them into the
+// one-byte-per-element shared-memory layout kind::f8f6f4 reads for E3M2/E2M3.
+// Its K extent must be the padded ld (a multiple of 128, zero-filled).
 int make_plane_map(CUtensorMap* map, const void* base, int elem_bytes, int64_t k, int64_t rows, int64_t planes,
-                   int64_t ld, int box_rows = 128) {
+                   int64_t ld, int box_rows = 128, bool fp6 = false) {
   EncodeFn enc = get_encode();
   if (!enc) return OZ_ETMAP;
   if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * elem_bytes) & 15)) return OZ_EINVAL;
-  const cuuint64_t dims[3] = {(cuuint64_t)k, (cuuint64_t)rows, (cuuint64_t)planes};
+  if (fp6 && ((reinterpret_cast<uintptr_t>(base) & 31) || (ld & 127))) return OZ_EINVAL;
+  const cuuint64_t dims[3] = {(cuuint64_t)(fp6 ? ld : k), (cuuint64_t)rows, (cuuint64_t)planes};
   const cuuint64_t strides[2] = {(cuuint64_t)(ld * elem_bytes), (cuuint64_t)(ld * elem_bytes * rows)};
   const cuuint32_t box[3] = {(cuuint32_t)(128 / elem_bytes), (cuuint32_t)box_rows, 1u};
   const cuuint32_t estr[3] = {1u, 1u, 1u};
+  const CUtensorMapDataType dt = fp6 ? CU_TENSOR_MAP_DATA_TYPE_16U6_ALIGN16B
+                                     : (elem_bytes == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16);
   const CUresult r =
-      enc(map, elem_bytes == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3,
+      enc(map, dt, 3,
           const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? OZ_OK : OZ_ETMAP;
@@ -306,6 +313,8 @@ int oz_split_fused(const double* X, int64_t rows, int64_t kb, int64_t ldx, int t
   P.X = X; P.rows = rows; P.kb = kb; P.ldx = ldx; P.rho = rho; P.cap = cap;
   P.coeff = static_cast<uint8_t*>(coeff); P.ld = ld_coeff; P.expo = expo; P.row_cnt = row_cnt;
   P.s_max = s_max; P.flags = flags; P.kmax = 1 << (53 - rho);
+  P.pack6 = (type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3) ? 1 : 0;
+  if (P.pack6 && (ld_coeff & 127)) return OZ_EINVAL;  // packed FP6 rows: multiples of 128 codes
   int rc = code_table(type2, f, rho, st, &P.table, &P.table_clean);
   if (rc) return rc;
   if (f.bytes == 1) return emu ? launch_fused_cfg<1, true>(P, st) : launch_fused_cfg<1, false>(P, st);
@@ -347,7 +356,7 @@ int oz_split_count(const double* X, int64_t rows, int64_t kb, int64_t ldx, int t
   uint32_t idf;
   if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
   if (rows < 0 || kb < 1 || ldx < kb || !X || !row_cnt || !s_max || !flags) return OZ_EINVAL;
-  const int64_t ld = (kb + 15) / 16 * 16;
+  const int64_t ld = (type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3) ? (kb + 127) / 128 * 128 : (kb + 15) / 16 * 16;
   return oz_split_fused(X, rows, kb, ldx, type2, rho, emu, 0, nullptr, ld, nullptr, row_cnt, s_max, flags, stream);
 }
 
@@ -397,10 +406,12 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   LpFormat f;
   uint32_t idf;
   if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
-  // FP6 slices: the split handles them (so fp6e2m3 reports SlicingInfeasible like
-  // the reference), but the byte-per-element operand layout is not what
-  // kind::f8f6f4 reads for E3M2/E2M3 (tools/fp6_probe.py) — not wired yet.
-  if (type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3) return OZ_EUNSUPPORTED;
+  // FP6: the split writes the packed 16U6_ALIGN16B layout, but the MMA path over
+  // it is not validated yet (tools/fp6_probe.py hung waiting on the TMA
+  // transaction count) — refuse rather than guess.  fp6e2m3 never gets here:
+  // the split reports SlicingInfeasible like the reference.
+  const bool fp6 = type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3;
+  if (fp6) return OZ_EUNSUPPORTED;
   if (m < 0 || n < 0 || kb < 1 || sx < 0 || sy < 0 || sx > planes_a || sy > planes_b || ldc < n || !C || !flags)
     return OZ_EINVAL;
   if ((tile_cnt_a == nullptr) != (tile_cnt_b == nullptr)) return OZ_EINVAL;
@@ -448,9 +459,9 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
     }
   }
   CUtensorMap ma, mb;
-  int rc = make_plane_map(&ma, a_planes, f.bytes, kb, m, planes_a, ld_a, oz::kPM);
+  int rc = make_plane_map(&ma, a_planes, f.bytes, kb, m, planes_a, ld_a, oz::kPM, fp6);
   if (rc) return rc;
-  rc = make_plane_map(&mb, b_planes, f.bytes, kb, n, planes_b, ld_b, tn / cta);
+  rc = make_plane_map(&mb, b_planes, f.bytes, kb, n, planes_b, ld_b, tn / cta, fp6);
   if (rc) return rc;
   P.tiles_m = pl.tiles_m;
   P.tiles_n = pl.tiles_n;
@@ -542,7 +553,7 @@ int oz_lp_gemm(const void* a_plane, const void* b_plane, int64_t ld_a, int64_t l
   LpFormat f;
   uint32_t idf;
   if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
-  if (type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3) return OZ_EUNSUPPORTED;  // see oz_pair_gemm
+  if (type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3) return OZ_EUNSUPPORTED;  // packed FP6: fused path only
   if (m < 0 || n < 0 || k < 0 || ldd < n || !D) return OZ_EINVAL;
   if (m == 0 || n == 0) return OZ_OK;
   cudaStream_t st = (cudaStream_t)stream;

@@ -94,6 +94,8 @@ struct FusedSplitParams {
   uint32_t* flags;
   const uint32_t* table;   // [2K+1] code | (not_representable << 16), index k + K
   int kmax;                // K = 2^(53-rho)
+  int pack6;               // FP6: 16 codes -> 12 packed bytes + 4 zero bytes per 16-byte group
+                           // (the TMA 16U6_ALIGN16B layout)
   int table_clean;         // 1: no entry carries the not-representable bit
 };
 
@@ -172,7 +174,7 @@ OZ_DEVICE uint64_t emu_slice_elem(uint64_t x, int g, int& k) {
 template <int kThreads, int kEPT, int kEB, bool kEmu, bool kWrite, bool kChecked>
 OZ_DEVICE uint32_t slice_iteration(uint64_t (&x)[kEPT], const uint64_t sigma, const int g, const uint32_t* __restrict__ tblc,
                                    int K, uint8_t* plane, int64_t base, int t, int64_t ld, uint32_t& flags,
-                                   uint32_t& bad) {
+                                   uint32_t& bad, const int pack6) {
   constexpr int kV = 16 / kEB;
   constexpr int kChunks = kEPT / kV;
   uint32_t key = 0;
@@ -213,7 +215,17 @@ OZ_DEVICE uint32_t slice_iteration(uint64_t (&x)[kEPT], const uint64_t sigma, co
       const int64_t e0 = base + ((int64_t)ch * kThreads + t) * kV;
       if (e0 < ld) {
         uint4 w;
-        if constexpr (kEB == 1) {
+        if (kEB == 1 && pack6) {
+          // 16 six-bit codes, little-endian bit order, into 96 bits; last word zero.
+          uint32_t q[3] = {0u, 0u, 0u};
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const uint32_t c6 = codes[u & (kV - 1)] & 63u, bit = 6u * (uint32_t)u;
+            q[bit >> 5] |= c6 << (bit & 31u);
+            if ((bit & 31u) > 26u) q[(bit >> 5) + 1] |= c6 >> (32u - (bit & 31u));
+          }
+          w = make_uint4(q[0], q[1], q[2], 0u);
+        } else if constexpr (kEB == 1) {
           w.x = __byte_perm(__byte_perm(codes[0], codes[1], 0x0040), __byte_perm(codes[2], codes[3], 0x0040), 0x5410);
           w.y = __byte_perm(__byte_perm(codes[4], codes[5], 0x0040), __byte_perm(codes[6], codes[7], 0x0040), 0x5410);
           w.z = __byte_perm(__byte_perm(codes[8], codes[9], 0x0040), __byte_perm(codes[10], codes[11], 0x0040), 0x5410);
@@ -330,13 +342,13 @@ __global__ void __launch_bounds__(kThreads, kThreads <= 256 ? 2 : 1) split_fused
     uint8_t* plane = row_plane0 + (int64_t)it * plane_stride;
     if (!write)
       key = slice_iteration<kThreads, kEPT, kEB, kEmu, false, true>(x, sigma, c + P.rho - 53, tblc, K, plane, base, t, P.ld,
-                                                                    flags, bad);
+                                                                    flags, bad, P.pack6);
     else if (checked)
       key = slice_iteration<kThreads, kEPT, kEB, kEmu, true, true>(x, sigma, c + P.rho - 53, tblc, K, plane, base, t, P.ld, flags,
-                                                                   bad);
+                                                                   bad, P.pack6);
     else
       key = slice_iteration<kThreads, kEPT, kEB, kEmu, true, false>(x, sigma, c + P.rho - 53, tblc, K, plane, base, t, P.ld,
-                                                                    flags, bad);
+                                                                    flags, bad, P.pack6);
     if (write && t == 0 && rank == 0) P.expo[(int64_t)it * P.rows + row] = c;
     ++cnt;
   }

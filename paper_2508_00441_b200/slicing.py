@@ -120,8 +120,39 @@ class DeviceSlices:
         """Codes as a [s, rows, kb] uint8/uint16 torch tensor view."""
         import torch
 
+        if self.fmt.name in ("fp6e3m2", "fp6e2m3"):
+            return torch.from_numpy(unpack_fp6(self.planes.cpu().numpy())[:, :, : self.kb])
         v = self.planes if _lib.ELEM_BYTES[self.fmt.name] == 1 else self.planes.view(torch.int16)
         return v[:, :, : self.kb]
+
+
+def _row_len(kb: int, fmt: FormatSpec) -> int:
+    """Elements per plane row: a multiple of 16 bytes, or of 128 codes for the
+    packed FP6 layout (16 six-bit codes per 16-byte group, TMA 16U6_ALIGN16B)."""
+    if fmt.name in ("fp6e3m2", "fp6e2m3"):
+        return -(-kb // 128) * 128
+    eb = _lib.ELEM_BYTES[fmt.name]
+    return -(-kb // (16 // eb)) * (16 // eb)
+
+
+def unpack_fp6(packed: np.ndarray) -> np.ndarray:
+    """[..., ld] bytes in 16-byte groups (12 bytes of little-endian 6-bit codes,
+    4 zero bytes) -> [..., ld] uint8 codes."""
+    g = packed.reshape(*packed.shape[:-1], -1, 16)[..., :12].astype(np.uint64)
+    lo = g[..., 0] | (g[..., 1] << 8) | (g[..., 2] << 16) | (g[..., 3] << 24) | (g[..., 4] << 32) | \
+        (g[..., 5] << 40) | (g[..., 6] << 48) | (g[..., 7] << 56)
+    hi = g[..., 8] | (g[..., 9] << 8) | (g[..., 10] << 16) | (g[..., 11] << 24)
+    out = np.empty(g.shape[:-1] + (16,), dtype=np.uint8)
+    for j in range(16):
+        b = 6 * j
+        if b + 6 <= 64:
+            v = (lo >> np.uint64(b)) & np.uint64(63)
+        elif b >= 64:
+            v = (hi >> np.uint64(b - 64)) & np.uint64(63)
+        else:
+            v = ((lo >> np.uint64(b)) | (hi << np.uint64(64 - b))) & np.uint64(63)
+        out[..., j] = v.astype(np.uint8)
+    return out.reshape(packed.shape)
 
 
 def _fmt_code(fmt: FormatSpec) -> int:
@@ -178,7 +209,7 @@ def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, str
         if X.dtype != torch.float64 or (X.stride(1) != 1 and kb > 1):
             raise ValueError("split expects a float64 view with unit column stride")
         ldx = X.stride(0) if rows > 1 else kb
-        ld = -(-kb // (16 // eb)) * (16 // eb)
+        ld = _row_len(kb, fmt)
         cap = _plane_cap(rows, ld * eb, predicted)
         row_cnt = torch.zeros(max(rows, 1), dtype=torch.int32, device=X.device)
         planes = torch.empty((cap, rows, ld * eb), dtype=torch.uint8, device=X.device)
@@ -244,7 +275,7 @@ def split_deferred(X, fmt: FormatSpec, params: SlicingParams, emu: bool, stream=
     if X.dtype != torch.float64 or (X.stride(1) != 1 and kb > 1):
         raise ValueError("split expects a float64 view with unit column stride")
     ldx = X.stride(0) if rows > 1 else kb
-    ld = -(-kb // (16 // eb)) * (16 // eb)
+    ld = _row_len(kb, fmt)
     cap = _plane_cap(rows, ld * eb, predict_slice_count(params) or 1)
     sf = torch.zeros(2, dtype=torch.int32, device=X.device)
     row_cnt = torch.empty(max(rows, 1), dtype=torch.int32, device=X.device)
