@@ -6,25 +6,29 @@
 //   ozgemm.py:192-193   T = ldexp(G, cA_p[i] + cB_q[j])     (_scale_terms_exact :132-140)
 //   ozgemm.py:194-197   Cb = Cb + T   (hardware FP64 or fp64emu.add_arrays)
 //   ozgemm.py:204-207   C  = C + Cb   (ascending blocks)
-// G never touches HBM.  Persistent, warp-specialised; each CTA owns 128 output
-// rows x 128 columns of C per tile, with its FP64 Cb in the registers of 8
-// epilogue warps.  Two variants:
-//   kCta = 1: one CTA per 128x128 tile, tcgen05.mma.cta_group::1 (M=128, N=128);
-//   kCta = 2: a CTA pair (cluster of 2) per 256x128 tile, tcgen05.mma.cta_group::2
-//             (M=256, N=128) issued by the leader; each CTA stages its 128 A rows
-//             and HALF the B tile, so per-SM operand ingest drops from 256 to
-//             192 rows per k-block and twice the pipeline stages fit in smem.
-// Roles (384 threads, 3 warpgroups; setmaxnreg moves registers to the epilogue):
-//   warp 0      TMA producer: A_p / B_q k-blocks (128 B rows, SWIZZLE_128B);
+// G never touches HBM.  Persistent, warp-specialised; the FP64 Cb of a tile stays
+// on chip (registers and/or TMEM) for all of its pairs.  Variants:
+//   kCta = 1: one CTA per 128 x 128 tile, tcgen05.mma.cta_group::1 (M = 128);
+//   kCta = 2: a CTA pair (cluster of 2) per 256 x kN tile, cta_group::2 (M = 256)
+//             issued by the leader; each CTA stages its 128 A rows and half of the
+//             B tile;
+//   kN = 192 (default for large problems): 2 TMEM accumulators, Cb columns
+//             [0,128) in registers and [128,192) in TMEM; kN = 128: 4 accumulators,
+//             Cb in registers (emulated mode: 2 accumulators, Cb all in TMEM).
+// Roles (384 threads; setmaxnreg moves registers to the epilogue):
+//   warp 0      TMA producer: A_p / B_q k-blocks (128 B rows, SWIZZLE_128B), paced
+//               across CTAs (below);
 //   warp 1      TMEM owner + tcgen05.mma issuer (kind::f8f6f4 or kind::f16, FP32
-//               accumulate) into one of 4 TMEM accumulators per pair;
-//   warps 4-11  epilogue: tcgen05.ld the FP32 G, rebuild T = G * 2^(eA+eB) as an
-//               FP64 bit pattern with integer ops (exact), and add it into the
-//               register-resident Cb in the reference pair order, with __dadd_rn
-//               (HW mode) or the integer-only emu_add (EMU mode — no DADD/DMUL/DFMA
-//               in that instantiation, tests/test_capi.py checks the SASS).
+//               accumulate, compile-time kind);
+//   warps 4-11  epilogue: tcgen05.ld the FP32 G, build T = G * 2^(eA+eB) as an FP64
+//               bit pattern with integer ops (exact), and add it into Cb in the
+//               reference pair order, with __dadd_rn (HW mode) or the integer-only
+//               add (EMU mode — no DADD/DMUL/DFMA in that instantiation,
+//               tests/test_capi.py checks the SASS).
 // Producers of all resident CTAs are paced to within `pace_slack` pair-steps of
 // each other so concurrently used slice panels stay L2-resident.
+// Performance note: DADDs only drain while the MMA warp waits for
+// an accumulator, so the epilogue work after a pair's first DADD is exposed.
 #include <climits>
 #include <type_traits>
 
