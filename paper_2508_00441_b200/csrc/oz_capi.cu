@@ -17,22 +17,17 @@ namespace {
 
 using oz::LpFormat;
 
-// Bit position of a 6-bit code inside its byte as the tensor core reads it
-// (OZ_FP6_SHIFT overrides, for the probe in tests/test_gpu_parity.py).
-int fp6_shift() {
-  static const int s = getenv("OZ_FP6_SHIFT") ? atoi(getenv("OZ_FP6_SHIFT")) : 0;
-  return s;
-}
-
 bool fmt_info(int type2, LpFormat& f, uint32_t& idesc_fmt) {
   switch (type2) {
     case OZ_FMT_E4M3: f = {4, 3, 7, 15, 1, 1, 0}; idesc_fmt = 0; return true;
     case OZ_FMT_E5M2: f = {5, 2, 15, 30, 0, 1, 0}; idesc_fmt = 1; return true;
     case OZ_FMT_FP16: f = {5, 10, 15, 30, 0, 2, 0}; idesc_fmt = 0; return true;
     case OZ_FMT_BF16: f = {8, 7, 127, 254, 0, 2, 0}; idesc_fmt = 1; return true;
-    // FP6 (OCP, no inf/NaN) in one byte per element, kind::f8f6f4 E3M2 = 4, E2M3 = 3.
-    case OZ_FMT_E3M2: f = {3, 2, 3, 7, 0, 1, fp6_shift()}; idesc_fmt = 4; return true;
-    case OZ_FMT_E2M3: f = {2, 3, 1, 3, 0, 1, fp6_shift()}; idesc_fmt = 3; return true;
+    // FP6 (OCP, no inf/NaN), kind::f8f6f4 E3M2 = 4, E2M3 = 3.  Slice planes hold the
+    // codes densely packed (6 bits each); TMA 16U6_ALIGN16B spreads every 16 codes
+    // to a 16-byte group in shared memory, the layout the MMA reads.
+    case OZ_FMT_E3M2: f = {3, 2, 3, 7, 0, 1, 0}; idesc_fmt = 4; return true;
+    case OZ_FMT_E2M3: f = {2, 3, 1, 3, 0, 1, 0}; idesc_fmt = 3; return true;
     default: return false;
   }
 }
@@ -81,7 +76,8 @@ int make_plane_map(CUtensorMap* map, const void* base, int elem_bytes, int64_t k
   if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * elem_bytes) & 15)) return OZ_EINVAL;
   if (fp6 && ((reinterpret_cast<uintptr_t>(base) & 31) || (ld & 127))) return OZ_EINVAL;
   const cuuint64_t dims[3] = {(cuuint64_t)(fp6 ? ld : k), (cuuint64_t)rows, (cuuint64_t)planes};
-  const cuuint64_t strides[2] = {(cuuint64_t)(ld * elem_bytes), (cuuint64_t)(ld * elem_bytes * rows)};
+  const int64_t row_bytes = fp6 ? ld * 3 / 4 : ld * elem_bytes;  // FP6 rows are densely packed
+  const cuuint64_t strides[2] = {(cuuint64_t)row_bytes, (cuuint64_t)(row_bytes * rows)};
   const cuuint32_t box[3] = {(cuuint32_t)(128 / elem_bytes), (cuuint32_t)box_rows, 1u};
   const cuuint32_t estr[3] = {1u, 1u, 1u};
   const CUtensorMapDataType dt = fp6 ? CU_TENSOR_MAP_DATA_TYPE_16U6_ALIGN16B
@@ -330,7 +326,8 @@ int oz_split_pad(void* coeff, int64_t ld_coeff, int64_t rows, int type2, int s, 
   if (rows == 0 || s == 0) return OZ_OK;
   if (!coeff || !expo || !row_cnt) return OZ_EINVAL;
   const unsigned blocks = (unsigned)((rows + 7) / 8);
-  oz::pad_planes_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<uint8_t*>(coeff), ld_coeff * f.bytes,
+  const int64_t row_bytes = (type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3) ? ld_coeff * 3 / 4 : ld_coeff * f.bytes;
+  oz::pad_planes_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<uint8_t*>(coeff), row_bytes,
                                                                    rows, s, expo, row_cnt, s_dev);
   return launch_status();
 }
@@ -406,12 +403,9 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   LpFormat f;
   uint32_t idf;
   if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
-  // FP6: the split writes the packed 16U6_ALIGN16B layout, but the MMA path over
-  // it is not validated yet (tools/fp6_probe.py hung waiting on the TMA
-  // transaction count) — refuse rather than guess.  fp6e2m3 never gets here:
-  // the split reports SlicingInfeasible like the reference.
+  // FP6 operands: packed planes, TMA 16U6_ALIGN16B (fp6e2m3 never gets here: the
+  // split reports SlicingInfeasible like the reference).
   const bool fp6 = type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3;
-  if (fp6) return OZ_EUNSUPPORTED;
   if (m < 0 || n < 0 || kb < 1 || sx < 0 || sy < 0 || sx > planes_a || sy > planes_b || ldc < n || !C || !flags)
     return OZ_EINVAL;
   if ((tile_cnt_a == nullptr) != (tile_cnt_b == nullptr)) return OZ_EINVAL;
@@ -435,6 +429,7 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   P.C = C; P.ldc = ldc; P.m = (int)m; P.n = (int)n; P.kb = (int)kb; P.sx = sx; P.sy = sy;
   P.order = order; P.cutoff = pair_cutoff; P.accumulate = accumulate;
   P.elem_bytes = f.bytes; P.fmt = idf; P.flags = flags; P.s_dev = s_dev;
+  P.fp6 = (type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3) ? 1 : 0;
   const PairPlan pl = plan_pair(m, n, sx, sy, pair_cutoff, emu);
   const int cta = pl.cta, tn = pl.tn;
   if (!workspace || (size_t)workspace_bytes < pl.eb_bytes) return OZ_EINVAL;  // see oz_pair_gemm_workspace

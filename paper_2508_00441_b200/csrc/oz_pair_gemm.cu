@@ -103,6 +103,7 @@ struct PairParams {
   int group;                 // raster band height in row-tiles
   uint64_t hint_a, hint_b;   // L2 cache policies of the operand loads
   uint32_t* band_done;       // [tiles_m / group] finished-tile counters (nullable)
+  int fp6;                   // operands are packed FP6 (TMA 16U6_ALIGN16B)
   unsigned long long* trace; // diagnostics (nullable): per-pair timestamps of unit 0
   int trace_cap;             // entries (pairs) the trace holds
   // Diagnostics only (OZ_DEBUG_MODE): bit 0 = epilogue skips the accumulation
@@ -570,11 +571,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
               const uint32_t st = it % kStages;
               if (it >= (uint32_t)kStages) mbar_wait(&s.empty[st], ((it / kStages) - 1) & 1);
               if constexpr (kCta == 1) {
-                mbar_arrive_expect_tx(&s.full[st], Cfg::kStageBytes);
+                mbar_arrive_expect_tx(&s.full[st], P.fp6 ? Cfg::kStageBytes / 4 * 3 : Cfg::kStageBytes);
                 tma_load_3d(s.a[st], &map_a, &s.full[st], kbi * kb_elems, arow, p, P.hint_a);
                 tma_load_3d(s.b[st], &map_b, &s.full[st], kbi * kb_elems, brow, q, P.hint_b);
               } else {
-                if (leader) mbar_arrive_expect_tx(&s.full[st], 2 * Cfg::kStageBytes);
+                if (leader)  // FP6: TMA signals the packed global bytes (96 per 128 codes)
+                  mbar_arrive_expect_tx(&s.full[st], P.fp6 ? 2 * Cfg::kStageBytes / 4 * 3 : 2 * Cfg::kStageBytes);
                 tma_load_3d_pair(s.a[st], &map_a, &s.full[st], kbi * kb_elems, arow, p, P.hint_a);
                 tma_load_3d_pair(s.b[st], &map_b, &s.full[st], kbi * kb_elems, brow, q, P.hint_b);
               }

@@ -94,8 +94,8 @@ struct FusedSplitParams {
   uint32_t* flags;
   const uint32_t* table;   // [2K+1] code | (not_representable << 16), index k + K
   int kmax;                // K = 2^(53-rho)
-  int pack6;               // FP6: 16 codes -> 12 packed bytes + 4 zero bytes per 16-byte group
-                           // (the TMA 16U6_ALIGN16B layout)
+  int pack6;               // FP6: 16 codes -> 12 densely packed bytes (rows of ld*3/4 bytes),
+                           // which TMA 16U6_ALIGN16B spreads to 16-byte groups in smem
   int table_clean;         // 1: no entry carries the not-representable bit
 };
 
@@ -224,7 +224,12 @@ OZ_DEVICE uint32_t slice_iteration(uint64_t (&x)[kEPT], const uint64_t sigma, co
             q[bit >> 5] |= c6 << (bit & 31u);
             if ((bit & 31u) > 26u) q[(bit >> 5) + 1] |= c6 >> (32u - (bit & 31u));
           }
-          w = make_uint4(q[0], q[1], q[2], 0u);
+          // Dense: 12 bytes per 16 codes (the global side of TMA 16U6_ALIGN16B).
+          uint32_t* dst = reinterpret_cast<uint32_t*>(plane + (e0 / 16) * 12);
+          dst[0] = q[0];
+          dst[1] = q[1];
+          dst[2] = q[2];
+          continue;
         } else if constexpr (kEB == 1) {
           w.x = __byte_perm(__byte_perm(codes[0], codes[1], 0x0040), __byte_perm(codes[2], codes[3], 0x0040), 0x5410);
           w.y = __byte_perm(__byte_perm(codes[4], codes[5], 0x0040), __byte_perm(codes[6], codes[7], 0x0040), 0x5410);
@@ -301,8 +306,9 @@ __global__ void __launch_bounds__(kThreads, kThreads <= 256 ? 2 : 1) split_fused
   const bool checked = __syncthreads_or(tiny) || !P.table_clean;
   if constexpr (kCL > 1) cluster_barrier();  // peers running before any DSMEM store
 
-  const int64_t plane_stride = P.rows * P.ld * kEB;  // bytes
-  uint8_t* const row_plane0 = P.coeff + row * P.ld * kEB;
+  const int64_t row_bytes = P.pack6 ? P.ld * 3 / 4 : P.ld * kEB;  // packed FP6: 6 bits per code
+  const int64_t plane_stride = P.rows * row_bytes;
+  uint8_t* const row_plane0 = P.coeff + row * row_bytes;
   const uint32_t* tblc = tbl + K;
   const bool write = P.coeff != nullptr;  // count-only mode otherwise (no planes, no exponents)
   int cnt = 0;

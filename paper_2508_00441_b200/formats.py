@@ -108,8 +108,7 @@ _E4M3_LUT = _minifloat_table(4, 3, 7)
 _E5M2_LUT = _minifloat_table(5, 2, 15)
 _E3M2_LUT = _minifloat_table(3, 2, 3)[:64]
 _E2M3_LUT = _minifloat_table(2, 3, 1)[:64]
-# Bit position of an FP6 code inside its byte (kept equal to the C library's).
-FP6_SHIFT = int(os.environ.get("OZ_FP6_SHIFT", "0"))
+FP6_SHIFT = 0  # FP6 codes are handled unpacked (slicing.unpack_fp6), one per byte
 
 
 def decode_codes(codes: np.ndarray, fmt_name: str) -> np.ndarray:

@@ -126,6 +126,13 @@ class DeviceSlices:
         return v[:, :, : self.kb]
 
 
+def _row_bytes(ld: int, fmt: FormatSpec) -> int:
+    """Bytes of one plane row of ld codes (packed FP6: 6 bits per code)."""
+    if fmt.name in ("fp6e3m2", "fp6e2m3"):
+        return ld * 3 // 4
+    return ld * _lib.ELEM_BYTES[fmt.name]
+
+
 def _row_len(kb: int, fmt: FormatSpec) -> int:
     """Elements per plane row: a multiple of 16 bytes, or of 128 codes for the
     packed FP6 layout (16 six-bit codes per 16-byte group, TMA 16U6_ALIGN16B)."""
@@ -136,9 +143,9 @@ def _row_len(kb: int, fmt: FormatSpec) -> int:
 
 
 def unpack_fp6(packed: np.ndarray) -> np.ndarray:
-    """[..., ld] bytes in 16-byte groups (12 bytes of little-endian 6-bit codes,
-    4 zero bytes) -> [..., ld] uint8 codes."""
-    g = packed.reshape(*packed.shape[:-1], -1, 16)[..., :12].astype(np.uint64)
+    """[..., ld*3/4] densely packed bytes (12 bytes of little-endian 6-bit codes
+    per 16 codes) -> [..., ld] uint8 codes."""
+    g = packed.reshape(*packed.shape[:-1], -1, 12).astype(np.uint64)
     lo = g[..., 0] | (g[..., 1] << 8) | (g[..., 2] << 16) | (g[..., 3] << 24) | (g[..., 4] << 32) | \
         (g[..., 5] << 40) | (g[..., 6] << 48) | (g[..., 7] << 56)
     hi = g[..., 8] | (g[..., 9] << 8) | (g[..., 10] << 16) | (g[..., 11] << 24)
@@ -152,7 +159,7 @@ def unpack_fp6(packed: np.ndarray) -> np.ndarray:
         else:
             v = ((lo >> np.uint64(b)) | (hi << np.uint64(64 - b))) & np.uint64(63)
         out[..., j] = v.astype(np.uint8)
-    return out.reshape(packed.shape)
+    return out.reshape(*packed.shape[:-1], packed.shape[-1] // 3 * 4)
 
 
 def _fmt_code(fmt: FormatSpec) -> int:
@@ -210,9 +217,9 @@ def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, str
             raise ValueError("split expects a float64 view with unit column stride")
         ldx = X.stride(0) if rows > 1 else kb
         ld = _row_len(kb, fmt)
-        cap = _plane_cap(rows, ld * eb, predicted)
+        cap = _plane_cap(rows, _row_bytes(ld, fmt), predicted)
         row_cnt = torch.zeros(max(rows, 1), dtype=torch.int32, device=X.device)
-        planes = torch.empty((cap, rows, ld * eb), dtype=torch.uint8, device=X.device)
+        planes = torch.empty((cap, rows, _row_bytes(ld, fmt)), dtype=torch.uint8, device=X.device)
         expo = torch.empty((cap, rows), dtype=torch.int32, device=X.device)
         if rows > 0:
             _lib.call("oz_split_fused", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu), cap,
@@ -233,7 +240,7 @@ def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, str
             flags &= 0xFFFFFFFF
             if check:
                 _lib.raise_for_flags(flags, "split")
-            planes = torch.empty((s_max, rows, ld * eb), dtype=torch.uint8, device=X.device)
+            planes = torch.empty((s_max, rows, _row_bytes(ld, fmt)), dtype=torch.uint8, device=X.device)
             expo = torch.empty((s_max, rows), dtype=torch.int32, device=X.device)
             if s_max > 0:
                 fw = torch.zeros(1, dtype=torch.int32, device=X.device)
@@ -276,10 +283,10 @@ def split_deferred(X, fmt: FormatSpec, params: SlicingParams, emu: bool, stream=
         raise ValueError("split expects a float64 view with unit column stride")
     ldx = X.stride(0) if rows > 1 else kb
     ld = _row_len(kb, fmt)
-    cap = _plane_cap(rows, ld * eb, predict_slice_count(params) or 1)
+    cap = _plane_cap(rows, _row_bytes(ld, fmt), predict_slice_count(params) or 1)
     sf = torch.zeros(2, dtype=torch.int32, device=X.device)
     row_cnt = torch.empty(max(rows, 1), dtype=torch.int32, device=X.device)
-    planes = torch.empty((cap, rows, ld * eb), dtype=torch.uint8, device=X.device)
+    planes = torch.empty((cap, rows, _row_bytes(ld, fmt)), dtype=torch.uint8, device=X.device)
     expo = torch.empty((cap, rows), dtype=torch.int32, device=X.device)
     if rows > 0:
         _lib.call("oz_split_fused", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu), cap,

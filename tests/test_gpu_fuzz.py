@@ -10,7 +10,8 @@ from conftest import bits, spread_matrix
 
 pytestmark = pytest.mark.gpu
 
-FMTS = [("fp8e4m3", "fp32"), ("fp8e4m3", "fp16"), ("fp16", "fp32"), ("bf16", "fp32"), ("fp8e5m2", "fp32")]
+FMTS = [("fp8e4m3", "fp32"), ("fp8e4m3", "fp16"), ("fp16", "fp32"), ("bf16", "fp32"), ("fp8e5m2", "fp32"),
+        ("fp6e3m2", "fp32")]
 
 
 def _case(seed):

@@ -221,24 +221,26 @@ def test_host_output_overlapped_copy(cuda, kbk):
 
 
 def test_fp6_formats(cuda):
-    """FP6 slices: the split is exact (fp6e3m2 planes bitwise vs the oracle) and
-    fp6e2m3 fails the reference's way (SlicingInfeasible, slicing.py:169-172);
-    fp6e3m2 slice products are not wired to tcgen05 yet (NotImplementedError,
-    tools/fp6_probe.py) — never a silent CPU path."""
+    """FP6 slices: packed 6-bit planes through TMA 16U6_ALIGN16B into kind::f8f6f4
+    E3M2 MMAs — fp6e3m2 slices and C bitwise equal to the oracle; fp6e2m3 fails the
+    reference's way (SlicingInfeasible, slicing.py:169-172)."""
     import oracle
 
     oz = _oz()
     rng = np.random.default_rng(66)
-    A = spread_matrix(rng, 40, 96, 0.5)
-    B = spread_matrix(rng, 96, 24, 0.5)
+    A = spread_matrix(rng, 300, 200, 0.5)
+    B = spread_matrix(rng, 200, 136, 0.5)
     f = oz.get_format("fp6e3m2")
-    params = oz.compute_params(53, f.mant_bits, 24, 96)
+    params = oz.compute_params(53, f.mant_bits, 24, 200)
     ss = oz.slice_matrix(A, "rows", f, params)
     coeff, expo, _, s, flags = oracle.split_rows(A, params.rho, False)
     assert flags == 0 and ss.s == s
     for p in range(s):
         assert np.array_equal(bits(ss.coeff[p]), bits(coeff[p]))
-    with pytest.raises(NotImplementedError):
-        oz.oz_gemm(A, B, oz.GemmConfig(f, oz.get_format("fp32")))
+    for kbk, emu in ((0, False), (64, False), (0, True)):
+        res = oz.oz_gemm(A, B, oz.GemmConfig(f, oz.get_format("fp32"), k_block=kbk, fp64_emulation=emu))
+        Cref, info = oracle.oz_gemm(A, B, "fp6e3m2", "fp32", kbk, emu)
+        assert [(b.k_lo, b.k_hi, b.s_x, b.s_y) for b in res.stats.blocks] == info["blocks"]
+        assert np.array_equal(bits(res.C), bits(Cref))
     with pytest.raises(oz.SlicingInfeasible):
         oz.oz_gemm(A, B, oz.GemmConfig(oz.get_format("fp6e2m3"), oz.get_format("fp32")))
