@@ -19,7 +19,7 @@
  * type2 codes (slice storage format, formats.py:85-100):
  *   OZ_FMT_E4M3 = 0 (fp8e4m3), OZ_FMT_E5M2 = 1 (fp8e5m2), OZ_FMT_FP16 = 2, OZ_FMT_BF16 = 3,
  *   OZ_FMT_E3M2 = 4 (fp6e3m2), OZ_FMT_E2M3 = 5 (fp6e2m3) — FP6 planes are densely packed (6 bits per
- *   code, rows of ld*3/4 bytes, ld a multiple of 128); oz_lp_gemm does not take FP6
+ *   code, rows of ld*3/4 bytes, ld a multiple of 128)
  */
 #ifndef OZ_B200_H
 #define OZ_B200_H

@@ -18,8 +18,9 @@ LIB_PATH = _HERE / "liboz_b200.so"
 OZ_OK, OZ_EINVAL, OZ_EUNSUPPORTED, OZ_ECUDA, OZ_ETMAP, OZ_ESLICES = range(6)
 FMT_CODE = {"fp8e4m3": 0, "fp8e5m2": 1, "fp16": 2, "bf16": 3, "fp6e3m2": 4, "fp6e2m3": 5}
 ELEM_BYTES = {"fp8e4m3": 1, "fp8e5m2": 1, "fp16": 2, "bf16": 2, "fp6e3m2": 1, "fp6e2m3": 1}
-# Slice formats whose products run on the tensor cores (FP6: split only, see oz_pair_gemm).
-TC_FORMATS = ("fp8e4m3", "fp8e5m2", "fp16", "bf16")
+# Slice formats whose products run on the tensor cores (fp6e2m3 slices are never
+# representable: SlicingInfeasible, as in the reference).
+TC_FORMATS = ("fp8e4m3", "fp8e5m2", "fp16", "bf16", "fp6e3m2")
 
 FLAG_NONFINITE_INPUT = 1 << 0
 FLAG_SUBNORMAL_INPUT = 1 << 1

@@ -548,7 +548,7 @@ int oz_lp_gemm(const void* a_plane, const void* b_plane, int64_t ld_a, int64_t l
   LpFormat f;
   uint32_t idf;
   if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
-  if (type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3) return OZ_EUNSUPPORTED;  // packed FP6: fused path only
+  const bool fp6 = type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3;  // packed planes, ld a multiple of 128
   if (m < 0 || n < 0 || k < 0 || ldd < n || !D) return OZ_EINVAL;
   if (m == 0 || n == 0) return OZ_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -558,14 +558,15 @@ int oz_lp_gemm(const void* a_plane, const void* b_plane, int64_t ld_a, int64_t l
   }
   if (!a_plane || !b_plane || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) return OZ_EINVAL;
   CUtensorMap ma, mb;
-  int rc = make_plane_map(&ma, a_plane, f.bytes, k, m, 1, ld_a);
+  int rc = make_plane_map(&ma, a_plane, f.bytes, k, m, 1, ld_a, 128, fp6);
   if (rc) return rc;
-  rc = make_plane_map(&mb, b_plane, f.bytes, k, n, 1, ld_b);
+  rc = make_plane_map(&mb, b_plane, f.bytes, k, n, 1, ld_b, 128, fp6);
   if (rc) return rc;
   const size_t smem = oz::tile_gemm_smem_bytes();
   cudaFuncSetAttribute(oz::tile_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const dim3 grid((unsigned)((m + oz::kTileM - 1) / oz::kTileM), (unsigned)((n + oz::kTileN - 1) / oz::kTileN));
-  oz::tile_gemm_kernel<<<grid, 128, smem, st>>>(ma, mb, D, ldd, (int)m, (int)n, (int)k, 0, 0, f.bytes, idf);
+  oz::tile_gemm_kernel<<<grid, 128, smem, st>>>(ma, mb, D, ldd, (int)m, (int)n, (int)k, 0, 0, f.bytes, idf,
+                                                 fp6 ? 1 : 0);
   return launch_status();
 }
 

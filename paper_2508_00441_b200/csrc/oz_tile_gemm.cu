@@ -33,7 +33,7 @@ struct TileSmem {
 __global__ void __launch_bounds__(128, 1)
     tile_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      float* __restrict__ D, int64_t ldd, int m, int n, int k, int plane_a, int plane_b,
-                     int elem_bytes, uint32_t fmt) {
+                     int elem_bytes, uint32_t fmt, int fp6) {
   extern __shared__ uint8_t smem_raw[];
   TileSmem& s = *reinterpret_cast<TileSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x / 32;
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(128, 1)
     for (int kb = 0; kb < num_kb; ++kb) {
       const int st = kb % kTileStages;
       if (kb >= kTileStages) mbar_wait(&s.empty[st], ((kb / kTileStages) - 1) & 1);
-      mbar_arrive_expect_tx(&s.full[st], 2 * kTileBytes);
+      mbar_arrive_expect_tx(&s.full[st], fp6 ? 2 * kTileBytes / 4 * 3 : 2 * kTileBytes);  // FP6: packed bytes
       tma_load_3d(s.a[st], &map_a, &s.full[st], kb * kb_elems, m0, plane_a, kEvictNormal);
       tma_load_3d(s.b[st], &map_b, &s.full[st], kb * kb_elems, n0, plane_b, kEvictNormal);
       mbar_wait(&s.full[st], (kb / kTileStages) & 1);

@@ -71,11 +71,39 @@ def encode_values(vals: np.ndarray, fmt: FormatSpec) -> np.ndarray:
         if not np.array_equal(f.astype(np.float64), vals) or np.any(bits & 0xFFFF):
             raise RepresentabilityError(f"matrix entries not representable in {fmt.name}")
         return (bits >> 16).astype(np.uint16)
-    raise NotImplementedError(f"no tensor-core operand path for {fmt.name} in this build")
+    raise NotImplementedError(f"no tensor-core operand path for {fmt.name} in this build")  # not reached for FP6
 
 
-def _padded_codes(torch, codes: np.ndarray):
+def _pack_fp6(codes: np.ndarray) -> np.ndarray:
+    """[rows, ld] 6-bit codes (ld a multiple of 16) -> [rows, ld*3/4] bytes, 16
+    codes per 12 bytes little-endian (the global side of TMA 16U6_ALIGN16B)."""
+    g = codes.reshape(codes.shape[0], -1, 16).astype(np.uint64)
+    lo = np.zeros(g.shape[:2], dtype=np.uint64)
+    hi = np.zeros(g.shape[:2], dtype=np.uint64)
+    for j in range(16):
+        b = 6 * j
+        v = g[..., j] & np.uint64(63)
+        if b < 64:
+            lo |= v << np.uint64(b)  # (bits past 63 fall off)
+        if b >= 64:
+            hi |= v << np.uint64(b - 64)
+        elif b + 6 > 64:  # straddles the two words
+            hi |= v >> np.uint64(64 - b)
+    out = np.empty(g.shape[:2] + (12,), dtype=np.uint8)
+    for i in range(8):
+        out[..., i] = ((lo >> np.uint64(8 * i)) & np.uint64(255)).astype(np.uint8)
+    for i in range(4):
+        out[..., 8 + i] = ((hi >> np.uint64(8 * i)) & np.uint64(255)).astype(np.uint8)
+    return out.reshape(codes.shape[0], -1)
+
+
+def _padded_codes(torch, codes: np.ndarray, fp6: bool = False):
     rows, k = codes.shape
+    if fp6:  # packed FP6 rows: ld a multiple of 128 codes
+        ld = -(-max(k, 1) // 128) * 128
+        buf = np.zeros((rows, ld), dtype=np.uint8)
+        buf[:, :k] = codes
+        return torch.from_numpy(_pack_fp6(buf)).cuda(), ld
     per16 = 16 // codes.itemsize
     ld = -(-max(k, 1) // per16) * per16
     buf = np.zeros((rows, ld), dtype=codes.dtype)
@@ -101,8 +129,9 @@ def lp_gemm(A: LpMatrix, B: LpMatrix, type3: FormatSpec) -> np.ndarray:
         return np.zeros((m, n))
     ca = encode_values(A.data, A.fmt)
     cb = encode_values(np.ascontiguousarray(B.data.T), B.fmt)  # K-major B
-    ta, lda = _padded_codes(torch, ca)
-    tb, ldb = _padded_codes(torch, cb)
+    fp6 = A.fmt.name in ("fp6e3m2", "fp6e2m3")
+    ta, lda = _padded_codes(torch, ca, fp6)
+    tb, ldb = _padded_codes(torch, cb, fp6)
     D = torch.empty((m, n), dtype=torch.float32, device="cuda")
     _lib.call("oz_lp_gemm", ta.data_ptr(), tb.data_ptr(), lda, ldb, m, n, k, _lib.FMT_CODE[A.fmt.name],
               D.data_ptr(), n, _lib.stream_ptr(torch))

@@ -244,3 +244,19 @@ def test_fp6_formats(cuda):
         assert np.array_equal(bits(res.C), bits(Cref))
     with pytest.raises(oz.SlicingInfeasible):
         oz.oz_gemm(A, B, oz.GemmConfig(oz.get_format("fp6e2m3"), oz.get_format("fp32")))
+
+
+def test_lp_gemm_fp6_exact(cuda):
+    """The lp_gemm seam (lpgemm.py:93-120) with packed FP6 operands: exact."""
+    oz = _oz()
+    rng = np.random.default_rng(12)
+    A = spread_matrix(rng, 130, 200, 0.5)
+    B = spread_matrix(rng, 200, 70, 0.5)
+    f = oz.get_format("fp6e3m2")
+    params = oz.compute_params(53, f.mant_bits, 24, 200)
+    sa = oz.slice_matrix(A, "rows", f, params)
+    sb = oz.slice_matrix(B, "cols", f, params)
+    for p in (0, sa.s - 1):
+        for q in (0, sb.s - 1):
+            G = oz.lp_gemm(oz.LpMatrix(sa.coeff[p], f), oz.LpMatrix(sb.coeff[q], f), oz.get_format("fp32"))
+            assert np.array_equal(G, sa.coeff[p] @ sb.coeff[q])

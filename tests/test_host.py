@@ -190,3 +190,19 @@ def test_fp64_level_summary_picks_fastest_accurate_variant():
     assert s["config"].startswith("pair_cutoff_11") and s["tflops"] == 30.0
     assert abs(s["vs_native_dgemm"] - 30.0 / 35.0) < 1e-12
     assert bench.fp64_level_summary({}) is None
+
+
+def test_fp6_pack_unpack_roundtrip():
+    """Host packer (lp_gemm seam) and unpacker (slice decode) of the dense FP6 layout."""
+    from paper_2508_00441_b200.lpgemm import _pack_fp6
+    from paper_2508_00441_b200.slicing import unpack_fp6
+
+    c = np.random.default_rng(1).integers(0, 64, size=(5, 256)).astype(np.uint8)
+    packed = _pack_fp6(c)
+    assert packed.shape == (5, 192)
+    assert np.array_equal(unpack_fp6(packed), c)
+    # bit order: code j of a group occupies bits [6j, 6j+6) little-endian
+    one = np.zeros((1, 16), np.uint8)
+    one[0, 10] = 63
+    v = int.from_bytes(_pack_fp6(one)[0].tobytes(), "little")
+    assert v == 63 << 60
