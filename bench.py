@@ -518,6 +518,7 @@ def run_variants(args, torch, oz, A, B, Cdd, d, nz, c_cublas, dev, steps=3):
         one(f"fp8_pair_cutoff_{cut}", oz.GemmConfig(f8, f32, pair_cutoff=cut), A, B, d, nz)
     one("fp8_emulated_fp64", oz.GemmConfig(f8, f32, fp64_emulation=True), A, B, d, nz)
     one("fp16_kblock1024_phi0.5", oz.GemmConfig(f16, f32, k_block=1024), A, B, d, nz)
+    one("fp6e3m2", oz.GemmConfig(oz.get_format("fp6e3m2"), f32), A, B, d, nz)
     # phi = 4 (wide exponent range): new inputs, own DD oracle and cuBLAS error
     A4, B4 = gpu_inputs(torch, n, n, n, 4.0, 4242, dev)
     Cdd4 = torch.empty((r, n), dtype=torch.float64, device=dev)
