@@ -29,6 +29,9 @@
 // each other so concurrently used slice panels stay L2-resident.
 // Performance note: DADDs only drain while the MMA warp waits for
 // an accumulator, so the epilogue work after a pair's first DADD is exposed.
+#ifndef OZ_TERM_FMA
+#define OZ_TERM_FMA 1  // HW-mode safe terms: DFMA(double(G), 2^(eA+eB), Cb) instead of bit assembly + DADD
+#endif
 #include <climits>
 #include <type_traits>
 
@@ -334,11 +337,12 @@ OZ_DEVICE void tmem_ld_wait_regs(uint32_t (&r)[16]) {
 // while the tensor cores run (profiles/microbench_r01.txt).  A zero term adds
 // +0, which leaves Cb unchanged (Cb is never -0: it starts at +0 and exact
 // cancellation gives +0).
-//   safe: every term of this (row, pair) is known to be normal (per-pair
-//   exponent bounds), so T = G * 2^(eA+eB) is assembled with 5 integer ops:
-//   FP32 bits >> 3 put G's exponent in the FP64 field, + (eA + eB + 896) << 20
-//   rebiases it (ea_sh, eb_sh pre-shifted), the sign is or-ed back, and the low
-//   word is G << 29.  Otherwise the checked make_term handles range errors.
+//   safe: every term of this (row, pair) and its scale 2^(eA+eB) are known to
+//   be normal (per-pair exponent bounds): one DFMA per element (OZ_TERM_FMA;
+//   =0 builds the bit-assembled T + DADD form: FP32 bits >> 3 put G's exponent
+//   in the FP64 field, + (eA + eB + 896) << 20 rebiases it, the sign is or-ed
+//   back, the low word is G << 29).  Otherwise the checked make_term handles
+//   range errors.
 //   Emulated mode: integer fast_add (emu_add for the rare operands it cannot take).
 template <bool kEmu>
 OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_sh, int ea_sh, bool safe, uint64_t* cb,
@@ -387,6 +391,23 @@ OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_sh, int e
   }
   uint64_t t[16];
   if (safe) {
+#if OZ_TERM_FMA
+    // Cb = fma(double(G), 2^(eA+eB), Cb): the product is exact (safe: normal
+    // term and normal scale), so the one rounding is that of Cb + T.  G = +-0
+    // gives a zero product, which leaves Cb (never -0) unchanged.
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int4 e4 = __ldg(ebv + v);
+      const int e[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double gd = (double)__uint_as_float(g[v * 4 + u]);
+        const double sc = __hiloint2double(ea_sh + e[u] + (127 << 20), 0);
+        cb[v * 4 + u] = d2u(__fma_rn(gd, sc, u2d(cb[v * 4 + u])));
+      }
+    }
+    return;
+#else
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int4 e4 = __ldg(ebv + v);
@@ -398,6 +419,7 @@ OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_sh, int e
         t[v * 4 + u] = ((gv << 1) != 0u) ? (((uint64_t)hi << 32) | (uint64_t)(gv << 29)) : 0ull;
       }
     }
+#endif
   } else {
     bool bad = false;
 #pragma unroll
@@ -679,7 +701,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
           const int ea_sh = (ea + 896) * (1 << 20);
           // Non-zero G has |G| in [2^-8, 2^17): FP32 exponent field in [119, 143].
           const int2 mm = __ldg(reinterpret_cast<const int2*>(P.ebmm) + (int64_t)q * P.tiles_n + tn);
-          const bool safe = ea + 896 + mm.x + 119 >= 1 && ea + 896 + mm.y + 143 <= 2046;
+          // (FMA terms also need the scale 2^(eA+eB) itself normal.)
+          const bool safe = ea + 896 + mm.x + 119 >= 1 && ea + 896 + mm.y + 143 <= 2046 &&
+                            (kEmu || !OZ_TERM_FMA || (ea + 1023 + mm.x >= 1 && ea + 1023 + mm.y <= 2046));
           const int32_t* ebq = P.ebsh + (int64_t)q * P.n_pad + tn * kN;
           // Pull this pair's B-exponent lines into L1 now: the loads that use them
           // come after the first DADD, i.e. in the short window in which the
