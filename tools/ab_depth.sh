@@ -1,4 +1,4 @@
-# A/B of MMA queue depth builds: liboz_d{0,2,3}.so built with -DOZ_MMA_DEPTH=0/2/3 (see oz_pair_gemm.cu).
+# A/B of MMA queue-depth builds liboz_d{0,2,3}.so (experiment patch, reverted: OZ_MMA_DEPTH no longer exists; see profiles/mma_depth_ab_r01.json).
 L=paper_2508_00441_b200/liboz_b200.so
 cp $L liboz_keep.so
 for r in 1 2; do
