@@ -138,7 +138,7 @@ extern "C" double micro_mma_rate(int cta, int n, int iters) {
 
 // ───────── contention probe: MMA issue (warp 0) concurrent with ALU/FP64 side work (warps 4-11) ─────────
 // side kind: 0 none, 1 DADD, 2 IADD64, 3 FFMA, 4 integer fast_add, 5 IMAD32
-template <int kSide>
+template <int kSide, int kN = 256>
 __global__ void __launch_bounds__(384, 1) mma_side(int mma_iters, int side_iters, unsigned long long* out) {
   extern __shared__ uint8_t raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(384, 1) mma_side(int mma_iters, int side_iters
   oz::tc_fence_after();
   if (warp == 0) {
     if (oz::elect_one() && mma_iters > 0) {
-      const uint32_t idesc = oz::make_idesc(0, 0, 128, 256);
+      const uint32_t idesc = oz::make_idesc(0, 0, 128, kN);
       const uint64_t ad = oz::smem_desc_sw128(a), bd = oz::smem_desc_sw128(b);
       long long t0 = clock64();
       for (int it = 0; it < mma_iters; ++it) {
@@ -201,15 +201,15 @@ __global__ void __launch_bounds__(384, 1) mma_side(int mma_iters, int side_iters
   if (warp == 0) oz::tmem_dealloc<512>(tbase);
 }
 
-template <int kSide>
+template <int kSide, int kN = 256>
 static void run_side(int mma_iters, int side_iters, double* mma_cyc, double* side_cyc) {
   const int grid = 148;
   unsigned long long* o;
   cudaMalloc(&o, sizeof(unsigned long long) * grid * 2);
   cudaMemset(o, 0, sizeof(unsigned long long) * grid * 2);
   const size_t smem = (128 + 256) * 128 + 2048;
-  cudaFuncSetAttribute(mma_side<kSide>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  mma_side<kSide><<<grid, 384, smem>>>(mma_iters, side_iters, o);
+  cudaFuncSetAttribute(mma_side<kSide, kN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  mma_side<kSide, kN><<<grid, 384, smem>>>(mma_iters, side_iters, o);
   cudaDeviceSynchronize();
   unsigned long long h[296];
   cudaMemcpy(h, o, sizeof(h), cudaMemcpyDeviceToHost);
@@ -232,5 +232,15 @@ extern "C" void micro_side(int side, int mma_iters, int side_iters, double* mma_
     default: run_side<5>(mma_iters, side_iters, &mc, &sc); break;
   }
   *mma_rate = mc > 0 ? (double)mma_iters * 4 * 128 * 256 * 32 / mc : 0;
+  *side_rate = sc > 0 ? 256.0 * 16 * side_iters / sc : 0;
+}
+
+// DADD side load against MMAs of width n (128 / 192 / 256; M = 128, cta_group::1).
+extern "C" void micro_side_n(int n, int mma_iters, int side_iters, double* mma_rate, double* side_rate) {
+  double mc = 0, sc = 0;
+  if (n == 128) run_side<1, 128>(mma_iters, side_iters, &mc, &sc);
+  else if (n == 192) run_side<1, 192>(mma_iters, side_iters, &mc, &sc);
+  else run_side<1, 256>(mma_iters, side_iters, &mc, &sc);
+  *mma_rate = mc > 0 ? (double)mma_iters * 4 * 128 * n * 32 / mc : 0;
   *side_rate = sc > 0 ? 256.0 * 16 * side_iters / sc : 0;
 }

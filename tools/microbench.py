@@ -47,6 +47,19 @@ def main(out=None):
             key = f"side_{name}_mma{int(mma_iters > 0)}_side{int(side_iters > 0)}"
             res[key] = {"mma_macs_per_clk_per_sm": mr.value, "side_ops_per_clk_per_sm": sr.value}
             print(f"{key}: MMA {mr.value:.0f} MAC/clk/SM, side {sr.value:.2f} op/clk/SM", flush=True)
+    # Is a DADD side load blocked for the whole MMA stream?  Side work small enough
+    # to finish well inside the MMA window: its duration should then be short.
+    lib.micro_side_n.restype = None
+    lib.micro_side_n.argtypes = lib.micro_side.argtypes
+    for n in (128, 192, 256):
+        for si in (250, 1000, 4000):
+            lib.micro_side_n(n, 20000, si, ctypes.byref(mr), ctypes.byref(sr))
+            mma_cyc = 20000 * 4 * 128 * n * 32 / mr.value if mr.value else 0
+            side_cyc = 256 * 16 * si / sr.value if sr.value else 0
+            key = f"window_dadd_n{n}_side{si}"
+            res[key] = {"mma_cycles": mma_cyc, "side_cycles": side_cyc, "side_ops": 256 * 16 * si,
+                        "side_cycles_alone_at_62.8": 256 * 16 * si / 62.8}
+            print(key, json.dumps(res[key]), flush=True)
     if out:
         Path(out).write_text(json.dumps(res, indent=1))
 
