@@ -163,22 +163,36 @@ def executed_pairs(tca, tcb, sx, sy, cutoff):
     return tot
 
 
-def cpu_baseline(args, rows, cols, n, threads=None):
+def sample_index(n, count, groups):
+    """`count` indices in `groups` runs of consecutive indices spread from the
+    first to the last row / column tile (several raster bands and tile waves)."""
+    width = max(1, count // groups)
+    starts = np.linspace(0, max(n - width, 0), groups).astype(int) // 8 * 8
+    starts[-1] = max(n - width, 0)
+    return np.unique(np.concatenate([np.arange(s, min(s + width, n)) for s in starts]))
+
+
+def cpu_baseline(args, rows, cols, n, threads=None, A=None, B=None):
     """Reference algorithm (C restatement, oracle/) on the host cores for a
     bounded sample: rows x cols of C at the full inner dimension n (same k, phi
-    and options as the GPU workload, so the slice structure matches)."""
+    and options as the GPU workload, so the slice structure matches).  With A
+    (rows x n) and B (n x cols) given — the GPU's own A rows and B columns — the
+    sample's C is also the parity check of the GPU's C block.  Returns the
+    summary and the sample's C."""
     import oracle
 
-    A, B = make_inputs(rows, n, cols, args.phi, 1234)
+    if A is None:
+        A, B = make_inputs(rows, n, cols, args.phi, 1234)
+    rows, cols = A.shape[0], B.shape[1]
     threads = threads or oracle.max_threads()
     t0 = time.perf_counter()
-    _, info = oracle.oz_gemm(A, B, args.type2, args.type3, args.kblock, args.emu, args.max_slices,
+    C, info = oracle.oz_gemm(A, B, args.type2, args.type3, args.kblock, args.emu, args.max_slices,
                              "smallest-first", args.pair_cutoff, nthreads=threads)
     dt = time.perf_counter() - t0
     return {"value": 2.0 * rows * cols * n / dt / 1e12, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"C[{rows}x{cols}] at k={n}, phi={args.phi}, {args.type2}/{args.type3} "
                       f"(reference algorithm, C restatement oracle/oz_oracle.c, {threads} threads)",
-            "seconds": dt, "blocks": info["blocks"]}
+            "seconds": dt, "blocks": info["blocks"], "flags": info["flags"]}, C
 
 
 def run_reference(args):
@@ -194,7 +208,7 @@ def run_reference(args):
     threads = oracle.max_threads()
     for _ in range(args.warmup):
         cpu_baseline(args, rows, cols, n, threads)
-    times = [cpu_baseline(args, rows, cols, n, threads) for _ in range(args.steps)]
+    times = [cpu_baseline(args, rows, cols, n, threads)[0] for _ in range(args.steps)]
     vals = [t["value"] for t in times]
     v = statistics.median(vals)
     ms = statistics.median([t["seconds"] for t in times]) * 1e3
@@ -349,7 +363,7 @@ def main():
 
     extras = {}
     if rank == 0 and not args.no_extras:
-        extras = run_extras(args, torch, oz, A, B, cfg, dev, world)
+        extras = run_extras(args, torch, oz, A, B, cfg, dev, world, Cbuf)
     # ---- e2e through the public API with host buffers (pinned) ----
     Ah = A.cpu().pin_memory()
     Bh = B.cpu().pin_memory()
@@ -406,13 +420,31 @@ def fp64_level_summary(extras):
             "vs_native_dgemm": tf / nat["tflops"]}
 
 
-def run_extras(args, torch, oz, A, B, cfg, dev, world=1):
+def run_extras(args, torch, oz, A, B, cfg, dev, world=1, C_gpu=None):
     """Accuracy vs the DD oracle, native cuBLAS DGEMM / FP8 on the same GPU,
-    and the CPU baseline (rank 0, N=1 leg)."""
+    and the CPU baseline + bitwise parity sample (rank 0, N=1 leg)."""
     from paper_2508_00441_b200 import _lib
 
     n = args.n
     out = {}
+    # Parity sample + CPU baseline: the oracle on the GPU's own A rows and B
+    # columns (spread over all raster bands / tile waves) must reproduce the
+    # timed run's C block bit for bit.
+    if world == 1 and C_gpu is not None:
+        rows = sample_index(n, args.cpu_rows, 4)
+        cols = sample_index(n, args.cpu_cols, 8)
+        ri, ci = torch.from_numpy(rows).to(dev), torch.from_numpy(cols).to(dev)
+        As = A.index_select(0, ri).cpu().numpy()
+        Bs = B.index_select(1, ci).cpu().numpy()
+        Cs = C_gpu.index_select(0, ri).index_select(1, ci).cpu().numpy()
+        cb, Cref = cpu_baseline(args, len(rows), len(cols), n, A=As, B=Bs)
+        nbad = int(np.sum(Cs.view(np.uint64) != Cref.view(np.uint64)))
+        out["parity"] = {"sample": f"C[{len(rows)}x{len(cols)}] of the timed run's C: rows in 4 runs, columns in 8 "
+                                   f"runs spread over all tile waves; oracle on the same A rows / B columns",
+                         "entries": int(Cs.size), "mismatches": nbad, "oracle_flags": cb["flags"],
+                         "bitwise_equal": nbad == 0 and cb.pop("flags") == 0}
+        cb.pop("blocks", None)
+        out["cpu_baseline"] = cb
     # native DGEMM
     C64 = torch.matmul(A, B)
     torch.cuda.synchronize()
@@ -461,13 +493,10 @@ def run_extras(args, torch, oz, A, B, cfg, dev, world=1):
                        "oracle": "double-double GEMM (oz_dd_gemm, TwoProd/TwoSum, one final rounding)",
                        "max_rel_err_ozaki": relerr(o), "max_rel_err_cublas_dgemm": relerr(c),
                        "ozaki_vs_cublas_max_abs_diff": float(np.max(np.abs(o - c)))}
-    single = world == 1  # variants and the CPU baseline: rank 0 at N = 1 only
+    single = world == 1  # variants: rank 0 at N = 1 only
     out["variants"] = run_variants(args, torch, oz, A, B, Cdd, d, nz, c, dev) \
         if single and not args.no_variants else None
     del C64, Cdd, Coz, C64r
-    if single:
-        out["cpu_baseline"] = cpu_baseline(args, args.cpu_rows, args.cpu_cols, n)
-        out["cpu_baseline"].pop("blocks", None)
     return out
 
 

@@ -138,6 +138,12 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
  * nothing to compute). */
 int64_t oz_pair_gemm_workspace(int64_t m, int64_t n, int sx, int sy, int pair_cutoff);
 
+/* Tuning override of oz_pair_gemm's kernel variant (no reference counterpart;
+ * results are bitwise identical in every variant): cta_group 1 | 2, tile_n
+ * 128 | 192, raster_group = row tiles per raster band; 0 = automatic (the
+ * default).  Process-wide; used by the variant tests and experiments. */
+int oz_set_pair_variant(int cta_group, int tile_n, int raster_group);
+
 /* One slice-pair product D (m x n, fp32) = A (m x k) . B (n x k)^T on tcgen05 —
  * replaces lpgemm.lp_gemm (lpgemm.py:93-120) for slice operands (exact). */
 int oz_lp_gemm(const void* a_plane, const void* b_plane, int64_t ld_a, int64_t ld_b, int64_t m, int64_t n,

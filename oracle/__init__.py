@@ -47,6 +47,8 @@ def _load():
         lib.oro_emu_add.restype = ctypes.c_uint64
         lib.oro_emu_add.argtypes = [ctypes.c_uint64, ctypes.c_uint64, P]
         lib.oro_max_threads.restype = I
+        lib.oro_dd_gemm.restype = None
+        lib.oro_dd_gemm.argtypes = [P, P, P, I64, I64, I64, I]
         _lib = lib
     return _lib
 
@@ -138,3 +140,26 @@ def oz_gemm(A, B, type2: str = "fp8e4m3", type3: str = "fp32", k_block: int = 0,
             C[:] = 0.0
         info["flags"] |= flags.value
     return C, info
+
+
+def dd_gemm(A, B, nthreads: int | None = None):
+    """Double-double GEMM with one final rounding (accuracy checker for the
+    acceptance criteria; pinned to the reference's exact ref_gemm by tests)."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    B = np.ascontiguousarray(B, dtype=np.float64)
+    m, k = A.shape
+    n = B.shape[1]
+    C = np.empty((m, n), dtype=np.float64)
+    _load().oro_dd_gemm(A.ctypes.data, B.ctypes.data, C.ctypes.data, m, n, k, nthreads or max_threads())
+    return C
+
+
+def naive_gemm(A, B):
+    """Triple-loop FP64 GEMM, ascending-k sequential accumulation (restates
+    oracle.naive_gemm_fp64, oracle.py:177-188)."""
+    A = np.asarray(A, dtype=np.float64)
+    B = np.asarray(B, dtype=np.float64)
+    C = np.zeros((A.shape[0], B.shape[1]))
+    for t in range(A.shape[1]):
+        C += A[:, t, None] * B[t, None, :]
+    return C

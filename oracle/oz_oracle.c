@@ -308,3 +308,50 @@ int oro_max_threads(void) {
   const long n = sysconf(_SC_NPROCESSORS_ONLN);
   return n > 0 ? (int)n : 1;
 }
+
+/* Accuracy checker for the acceptance criteria 6/7 (pkg/tests/test_acceptance.py:
+ * 201-250), standing in for the reference's exact ref_gemm (oracle.py:150-174):
+ * every dot product accumulated in double-double (TwoProd via fma, TwoSum),
+ * rounded once.  Not exact in general, so tests pin it bitwise to ref_gemm's
+ * output on the criteria's own inputs (tests/golden/accept.json). */
+typedef struct {
+  const double* A; const double* B; double* C; int64_t m, n, k;
+  int64_t next; pthread_mutex_t mu;
+} DDJob;
+
+static void* dd_worker(void* arg) {
+  DDJob* J = (DDJob*)arg;
+  for (;;) {
+    pthread_mutex_lock(&J->mu);
+    const int64_t i = J->next++;
+    pthread_mutex_unlock(&J->mu);
+    if (i >= J->m) break;
+    for (int64_t j = 0; j < J->n; ++j) {
+      double hi = 0.0, lo = 0.0;
+      for (int64_t t = 0; t < J->k; ++t) {
+        const double a = J->A[i * J->k + t], b = J->B[t * J->n + j];
+        const double p = a * b, pe = fma(a, b, -p);
+        const double s = hi + p, bb = s - hi, se = (hi - (s - bb)) + (p - bb);
+        lo += se + pe;
+        hi = s;
+      }
+      const double r = hi + lo;
+      J->C[i * J->n + j] = r;
+    }
+  }
+  return NULL;
+}
+
+void oro_dd_gemm(const double* A, const double* B, double* C, int64_t m, int64_t n, int64_t k, int nthreads) {
+  DDJob J;
+  memset(&J, 0, sizeof J);
+  J.A = A; J.B = B; J.C = C; J.m = m; J.n = n; J.k = k;
+  pthread_mutex_init(&J.mu, NULL);
+  if (nthreads < 1) nthreads = 1;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * nthreads);
+  for (int i = 1; i < nthreads; ++i) pthread_create(&th[i], NULL, dd_worker, &J);
+  dd_worker(&J);
+  for (int i = 1; i < nthreads; ++i) pthread_join(th[i], NULL);
+  pthread_mutex_destroy(&J.mu);
+  free(th);
+}

@@ -46,6 +46,7 @@ SIGNATURES = {
     "oz_pair_gemm": (_I, [_P, _P, _I64, _I64, _I, _I, _P, _P, _P, _P, _I64, _I64, _I64, _I, _I, _I,
                           _I, _I, _I, _I, _P, _I64, _P, _P, _I64, _I, _P, _I64, _P, _P, _P]),
     "oz_pair_gemm_workspace": (ctypes.c_int64, [_I64, _I64, _I, _I, _I]),
+    "oz_set_pair_variant": (_I, [_I, _I, _I]),
     "oz_lp_gemm": (_I, [_P, _P, _I64, _I64, _I64, _I64, _I64, _I, _P, _I64, _P]),
     "oz_emu_add_batch": (_I, [_P, _P, _P, _I64, _I, _P, _P]),
     "oz_dd_gemm": (_I, [_P, _P, _P, _I64, _I64, _I64, _P]),
@@ -103,6 +104,12 @@ def require_cuda():
         raise BackendUnavailable("no CUDA device: the B200 backend has no CPU fallback")
     load()
     return torch
+
+
+def set_pair_variant(cta_group: int = 0, tile_n: int = 0, raster_group: int = 0) -> None:
+    """Force oz_pair_gemm's kernel variant (0 = automatic).  Results are bitwise
+    identical in every variant; tests use this to cover all of them."""
+    call("oz_set_pair_variant", cta_group, tile_n, raster_group)
 
 
 def stream_ptr(torch) -> int:

@@ -6,6 +6,7 @@
 #include "oz_split.cu"
 #include "oz_dd_gemm.cu"
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -237,15 +238,19 @@ struct PairPlan {
   size_t eb_bytes, band_bytes, pace_bytes;
 };
 
+// Tuning overrides (oz_set_pair_variant; 0 = automatic).  Process-wide, set
+// once by experiments and the variant tests — never read from the environment.
+std::atomic<int> g_force_cta{0}, g_force_tn{0}, g_force_group{0};
+
 PairPlan plan_pair(int64_t m, int64_t n, int sx, int sy, int pair_cutoff, int emu) {
   PairPlan pl{};
   // CTA pair (cta_group::2) unless the problem has a single 128-row slab; N = 192
   // columns per pair tile in hardware-FP64 mode (tensor-bound), N = 128 in the
   // emulated mode (ALU-bound epilogue: 4 accumulators absorb its jitter, and all
   // of Cb sits in registers; measured 144 -> 109 ms at n = 8192, pair_cutoff = 11).
-  // OZ_CTA_GROUP=1|2 and OZ_TILE_N=128|192 override (experiments, tests).
+  // oz_set_pair_variant(cta_group, tile_n, group) overrides (experiments, tests).
   pl.cta = m > oz::kPM ? 2 : 1;
-  if (const char* e = getenv("OZ_CTA_GROUP")) pl.cta = atoi(e) == 1 ? 1 : 2;
+  if (const int f = g_force_cta.load(std::memory_order_relaxed)) pl.cta = f == 1 ? 1 : 2;
   pl.tn = 128;
   if (pl.cta == 2 && n > 128 && !emu) {
     // N = 192 unless tile quantisation favours N = 128: time ~ waves x N / efficiency,
@@ -256,7 +261,7 @@ PairPlan plan_pair(int64_t m, int64_t n, int sx, int sy, int pair_cutoff, int em
     const int64_t w128 = (tm * ((n + 127) / 128) + units - 1) / units;
     pl.tn = (double)w192 * 192.0 <= (double)w128 * 128.0 * 1.07 ? 192 : 128;
   }
-  if (const char* e = getenv("OZ_TILE_N")) pl.tn = (atoi(e) == 192 && pl.cta == 2 && !emu) ? 192 : 128;
+  if (const int f = g_force_tn.load(std::memory_order_relaxed)) pl.tn = (f == 192 && pl.cta == 2 && !emu) ? 192 : 128;
   pl.tiles_m = (int)((m + oz::kPM * pl.cta - 1) / (oz::kPM * pl.cta));
   pl.tiles_n = (int)((n + pl.tn - 1) / pl.tn);
   pl.pairs = 0;
@@ -267,7 +272,7 @@ PairPlan plan_pair(int64_t m, int64_t n, int sx, int sy, int pair_cutoff, int em
   pl.eb_bytes = (sizeof(int32_t) * (size_t)sy * (n_pad + 2 * (size_t)pl.tiles_n) + 255) / 256 * 256;
   pl.pace_bytes = sizeof(uint32_t) * (size_t)pl.tiles_m * pl.tiles_n * (size_t)pl.pairs;
   pl.group = 8;
-  if (const char* e = getenv("OZ_GROUP")) pl.group = atoi(e) > 0 ? atoi(e) : 8;
+  if (const int f = g_force_group.load(std::memory_order_relaxed)) pl.group = f;
   pl.bands = (pl.tiles_m + pl.group - 1) / pl.group;
   pl.band_bytes = (sizeof(uint32_t) * (size_t)pl.bands + 255) / 256 * 256;
   return pl;
@@ -330,6 +335,15 @@ int oz_split_pad(void* coeff, int64_t ld_coeff, int64_t rows, int type2, int s, 
   oz::pad_planes_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<uint8_t*>(coeff), row_bytes,
                                                                    rows, s, expo, row_cnt, s_dev);
   return launch_status();
+}
+
+int oz_set_pair_variant(int cta_group, int tile_n, int raster_group) {
+  if (cta_group < 0 || cta_group > 2 || (tile_n != 0 && tile_n != 128 && tile_n != 192) || raster_group < 0)
+    return OZ_EINVAL;
+  g_force_cta.store(cta_group, std::memory_order_relaxed);
+  g_force_tn.store(tile_n, std::memory_order_relaxed);
+  g_force_group.store(raster_group, std::memory_order_relaxed);
+  return OZ_OK;
 }
 
 const char* oz_version(void) { return "oz_b200 0.1 (sm_100a tcgen05; reference ozdgemm 1.0.0 semantics)"; }
@@ -433,8 +447,20 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   const PairPlan pl = plan_pair(m, n, sx, sy, pair_cutoff, emu);
   const int cta = pl.cta, tn = pl.tn;
   if (!workspace || (size_t)workspace_bytes < pl.eb_bytes) return OZ_EINVAL;  // see oz_pair_gemm_workspace
+  P.group = pl.group;
+  P.hint_a = P.hint_b = oz::kEvictNormal;
+  // Non-zero G: FP32 exponent field in [127 - 2 m2, 127 + ceil(log2 kb)] (PairParams).
+  P.g_lo = 127 - 2 * (f.mbits + 1);
+  {
+    int lg = 0;
+    while ((1ll << lg) < kb) ++lg;
+    P.g_hi = 127 + lg;
+  }
+  P.trace = nullptr; P.trace_cap = 0; P.debug = 0;
+#if OZ_DIAGNOSTICS
+  // Diagnostic builds only (tools/): OZ_DEBUG_MODE bits, L2 hints, and
+  // OZ_TRACE=<device address hex>:<entries> (tools/k3_trace.py).
   if (const char* e = getenv("OZ_DEBUG_MODE")) P.debug = atoi(e);
-  P.group = 8;
   {
     const uint64_t hints[3] = {oz::kEvictNormal, oz::kEvictFirst, oz::kEvictLast};
     const char* ha = getenv("OZ_HINT_A");
@@ -442,9 +468,6 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
     P.hint_a = hints[ha ? (atoi(ha) % 3 + 3) % 3 : 0];
     P.hint_b = hints[hb ? (atoi(hb) % 3 + 3) % 3 : 0];
   }
-  if (const char* e = getenv("OZ_GROUP")) P.group = atoi(e) > 0 ? atoi(e) : 8;
-  // Diagnostics: OZ_TRACE=<device address hex>:<entries> (tools/k3_trace.py).
-  P.trace = nullptr; P.trace_cap = 0;
   if (const char* e = getenv("OZ_TRACE")) {
     unsigned long long addr = 0;
     int cap = 0;
@@ -453,6 +476,7 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
       P.trace_cap = cap;
     }
   }
+#endif
   CUtensorMap ma, mb;
   int rc = make_plane_map(&ma, a_planes, f.bytes, kb, m, planes_a, ld_a, oz::kPM, fp6);
   if (rc) return rc;

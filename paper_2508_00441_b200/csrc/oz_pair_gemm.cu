@@ -32,6 +32,9 @@
 #ifndef OZ_TERM_FMA
 #define OZ_TERM_FMA 1  // HW-mode safe terms: DFMA(double(G), 2^(eA+eB), Cb) instead of bit assembly + DADD
 #endif
+#ifndef OZ_DIAGNOSTICS
+#define OZ_DIAGNOSTICS 0  // 1: per-pair clock trace + OZ_DEBUG_MODE hooks (tools/ only; never the product)
+#endif
 #include <climits>
 #include <type_traits>
 
@@ -107,10 +110,15 @@ struct PairParams {
   uint64_t hint_a, hint_b;   // L2 cache policies of the operand loads
   uint32_t* band_done;       // [tiles_m / group] finished-tile counters (nullable)
   int fp6;                   // operands are packed FP6 (TMA 16U6_ALIGN16B)
-  unsigned long long* trace; // diagnostics (nullable): per-pair timestamps of unit 0
+  // FP32 exponent-field range of a non-zero G: coefficients sit on the grid
+  // 2^(rho-53) >= 2^-m2 with |c| <= 1, so 2^(-2 m2) <= |G| <= kb, i.e. the field is in
+  // [127 - 2 m2, 127 + ceil(log2 kb)].  The epilogue's fast (unchecked) term path is
+  // taken only when every term of a (row, pair) is then provably normal.
+  int g_lo, g_hi;
+  unsigned long long* trace; // diagnostics (OZ_DIAGNOSTICS builds only): per-pair timestamps of unit 0
   int trace_cap;             // entries (pairs) the trace holds
-  // Diagnostics only (OZ_DEBUG_MODE): bit 0 = epilogue skips the accumulation
-  // (MMA-only timing), bit 3 = no C stores.  Results are wrong with either.
+  // Diagnostics only (OZ_DIAGNOSTICS builds, OZ_DEBUG_MODE): bit 0 = epilogue skips the
+  // accumulation (MMA-only timing), bit 3 = no C stores.  Results are wrong with either.
   int debug;
 };
 
@@ -440,7 +448,9 @@ OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_sh, int e
 template <bool kEmu, typename Acc>
 OZ_DEVICE void store_row(const PairParams& P, int row, int col0, const Acc* cb, int cnt, uint32_t& flags) {
   Acc* crow = reinterpret_cast<Acc*>(P.C) + (int64_t)row * P.ldc + col0;
-  const bool vec = ((P.ldc & 1) == 0) && ((col0 & 1) == 0) && (col0 + cnt <= P.n);
+  // 16-byte stores only where this row segment is 16-byte aligned (callers may
+  // pass C views at odd column offsets or 8-byte-aligned pointers).
+  const bool vec = ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) && (col0 + cnt <= P.n);
   if (vec) {
     using Acc2 = ulonglong2;
 #pragma unroll
@@ -618,7 +628,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         PairIter pi;
         for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
           const uint32_t buf = acc_it % kAccBufs;
-          const bool tr = P.trace && unit == 0 && acc_it < (uint32_t)P.trace_cap;
+          const bool tr = OZ_DIAGNOSTICS && P.trace && unit == 0 && acc_it < (uint32_t)P.trace_cap;
           long long full_wait = 0;
           if (tr && lane == 0) P.trace[acc_it * 8 + 0] = clock64();
           if (acc_it >= (uint32_t)kAccBufs) mbar_wait(&s.acc_empty[buf], ((acc_it / kAccBufs) - 1) & 1);
@@ -689,20 +699,21 @@ __global__ void __launch_bounds__(kPThreads, 1)
       for (pi.init(lp_walk, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
         const int p = pi.p, q = pi.q();
         const uint32_t buf = acc_it % kAccBufs;
-        const bool tr = P.trace && unit == 0 && crank == 0 && warp == 4 && lane == 0 && acc_it < (uint32_t)P.trace_cap;
+        const bool tr = OZ_DIAGNOSTICS && P.trace && unit == 0 && crank == 0 && warp == 4 && lane == 0 &&
+                         acc_it < (uint32_t)P.trace_cap;
         if (tr) P.trace[acc_it * 8 + 3] = clock64();
         mbar_wait(&s.acc_full[buf], (acc_it / kAccBufs) & 1);
         if (tr) P.trace[acc_it * 8 + 4] = clock64();
         tc_fence_after();
         // p >= lp: this CTA's rows have an all-zero A slice p (the partner needs it):
         // the term is +0, nothing to add.
-        if (p < lp && !(P.debug & 1)) {
+        if (p < lp && !(OZ_DIAGNOSTICS && (P.debug & 1))) {
           const int ea = row < P.m ? __ldg(P.expo_a + (int64_t)p * P.m + row) : 0;
           const int ea_sh = (ea + 896) * (1 << 20);
-          // Non-zero G has |G| in [2^-8, 2^17): FP32 exponent field in [119, 143].
+          // Non-zero G has its FP32 exponent field in [g_lo, g_hi] (PairParams).
           const int2 mm = __ldg(reinterpret_cast<const int2*>(P.ebmm) + (int64_t)q * P.tiles_n + tn);
           // (FMA terms also need the scale 2^(eA+eB) itself normal.)
-          const bool safe = ea + 896 + mm.x + 119 >= 1 && ea + 896 + mm.y + 143 <= 2046 &&
+          const bool safe = ea + 896 + mm.x + P.g_lo >= 1 && ea + 896 + mm.y + P.g_hi <= 2046 &&
                             (kEmu || !OZ_TERM_FMA || (ea + 1023 + mm.x >= 1 && ea + 1023 + mm.y <= 2046));
           const int32_t* ebq = P.ebsh + (int64_t)q * P.n_pad + tn * kN;
           // Pull this pair's B-exponent lines into L1 now: the loads that use them
@@ -764,7 +775,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
       // C = Cb (first block) or C = C + Cb (ozgemm.py:204-207).  The TMEM reads
       // are warp-collective (.sync.aligned): issue them outside the row guard.
-      const bool store = !(P.debug & 8);  // diagnostics: bit 3 skips the C stores
+      const bool store = !(OZ_DIAGNOSTICS && (P.debug & 8));  // diagnostics: bit 3 skips the C stores
       if constexpr (kRegCols > 0)
         if (row < P.m && store) store_row<kEmu>(P, row, tn * kN + half * 64, cb, 64, flags);
       if constexpr (kTmHalf > 0) {

@@ -100,13 +100,22 @@ struct FusedSplitParams {
 };
 
 // table[k + K] = code of k * 2^(rho-53) (| 1<<16 if not representable).
+// Integer only (it also runs for the emulated-FP64 path, whose kernels must
+// contain no FP64 instruction): the FP64 bits of k * 2^(rho-53) are assembled
+// from the normalised |k| (|k| <= 2^11, so the value is exact and normal).
 __global__ void build_code_table_kernel(uint32_t* table, int kmax, int rho, LpFormat f) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i > 2 * kmax) return;
   const int k = i - kmax;
   uint32_t fl = 0;
-  const double v = (double)k * ldexp(1.0, rho - 53);
-  const uint32_t code = encode_coeff(d2u(v), 0, f, fl);
+  uint64_t vb = 0;
+  if (k != 0) {
+    const uint32_t a = (uint32_t)(k < 0 ? -k : k);
+    const int pos = 31 - __clz((int)a);  // |k| = 1.f * 2^pos
+    vb = ((uint64_t)(k < 0) << 63) | ((uint64_t)(pos + rho - 53 + 1023) << 52) |
+         (((uint64_t)a << (52 - pos)) & kFracMask);
+  }
+  const uint32_t code = encode_coeff(vb, 0, f, fl);
   table[i] = code | (fl ? (1u << 16) : 0u);
 }
 

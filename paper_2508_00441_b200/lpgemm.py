@@ -112,8 +112,50 @@ def _padded_codes(torch, codes: np.ndarray, fp6: bool = False):
     return t, ld
 
 
+def _lsb_exponent(M: np.ndarray):
+    """Smallest exponent e with every non-zero entry a multiple of 2^e, and the
+    largest magnitude (None, 0 for an all-zero matrix)."""
+    v = np.abs(M[M != 0])
+    if v.size == 0:
+        return None, 0.0
+    bits = v.view(np.uint64)
+    field = (bits >> np.uint64(52)).astype(np.int64)
+    sig = (bits & np.uint64((1 << 52) - 1)) | np.where(field > 0, np.uint64(1 << 52), np.uint64(0))
+    tz = np.zeros(sig.shape, dtype=np.int64)
+    s = sig.copy()
+    for sh in (32, 16, 8, 4, 2, 1):  # count trailing zeros of the significand
+        low = (s & np.uint64((1 << sh) - 1)) == 0
+        tz += np.where(low, sh, 0)
+        s = np.where(low, s >> np.uint64(sh), s)
+    return int(np.min(np.maximum(field, 1) - 1075 + tz)), float(v.max())
+
+
+def accumulation_is_exact(A: np.ndarray, B: np.ndarray, type3: FormatSpec) -> bool:
+    """True when every partial sum of A @ B, in any order, is exactly
+    representable both in type3 and in the tensor cores' FP32 accumulator.
+    Then the reference's per-step type3 RNE accumulation (lpgemm.py:49-77,
+    105-119) and tcgen05's FP32 accumulation both produce the exact product, so
+    they agree bit for bit.  All products are multiples of 2^(ga + gb) and every
+    partial sum is bounded by k * max|A| * max|B|."""
+    k = A.shape[1]
+    ga, ma = _lsb_exponent(A)
+    gb, mb = _lsb_exponent(B)
+    if ga is None or gb is None or k == 0:
+        return True
+    g = ga + gb
+    bound = k * ma * mb
+    width = min(type3.mant_bits, 24)
+    return (bound <= 2.0 ** (g + width)           # N * 2^g with |N| <= 2^m3 fits the significand
+            and g >= type3.exp_min - type3.mant_bits + 1 and g >= -126  # grid above the subnormal quantum
+            and bound <= type3.max_finite and bound < 2.0 ** 127)
+
+
 def lp_gemm(A: LpMatrix, B: LpMatrix, type3: FormatSpec) -> np.ndarray:
-    """C = A @ B with FP32 tensor-core accumulation (exact on slice operands)."""
+    """C = A @ B on the tensor cores (FP32 accumulation in TMEM).  Defined
+    exactly where the reference's per-step type3-rounded result is the exact
+    product (always true for slice operands, the pipeline's only use); other
+    operands raise NotImplementedError instead of returning a differently
+    rounded result."""
     if A.shape[1] != B.shape[0]:
         raise ValueError("inner dimensions do not match")
     if 2 * max(A.fmt.mant_bits, B.fmt.mant_bits) > 53:
@@ -122,6 +164,10 @@ def lp_gemm(A: LpMatrix, B: LpMatrix, type3: FormatSpec) -> np.ndarray:
         raise NotImplementedError("mixed operand formats are not wired to tcgen05 in this build")
     if type3.mant_bits > 24:
         raise NotImplementedError("accumulators wider than FP32 are not available on the tensor cores")
+    if not accumulation_is_exact(A.data, B.data, type3):
+        raise NotImplementedError(
+            f"lp_gemm: this product's {type3.name} accumulation can round; the tensor-core path computes "
+            "exact products only (per-step type3 rounding, lpgemm.py:49-77, is not implemented)")
     torch = _lib.require_cuda()
     m, k = A.shape
     n = B.shape[1]

@@ -190,11 +190,13 @@ def _panel_plan(m: int, n: int, kb: int, eb: int, torch) -> tuple[int, int]:
         return mp, np_
     free, _ = torch.cuda.mem_get_info()
     budget = max(free - PANEL_MARGIN_BYTES, 1 << 30)
+    # Halve the larger extent, keeping panels multiples of 128 (whole MMA tiles,
+    # and 16-byte aligned C column offsets for the vectorised epilogue stores).
     while need(mp, np_) > budget and (mp > 256 or np_ > 256):
         if np_ >= mp:
-            np_ = max(256, -(-np_ // 2))
+            np_ = max(256, -(-np_ // 256) * 128)
         else:
-            mp = max(256, -(-mp // 2))
+            mp = max(256, -(-mp // 256) * 128)
     return mp, np_
 
 
@@ -226,12 +228,15 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
     stats = OzStats()
     C = out if out is not None else torch.empty((m, n), dtype=torch.float64, device=A.device)
     sp = _lib.stream_ptr(torch)
-    flags = torch.zeros(1, dtype=torch.int32, device=A.device)
+    kblocks = _blocks(k, cfg.k_block)
+    # One GEMM flag word per k-block, so errors are raised in the reference's
+    # order: block by block, A's split, B's split, then that block's terms/adds.
+    gflags = torch.zeros(max(len(kblocks), 1), dtype=torch.int32, device=A.device)
     evs = []  # (split start, split end, gemm end) per pass
     eb = _lib.ELEM_BYTES.get(cfg.type2.name, 1)
     mp, np_ = m, n
-    blocks = []  # per block: (lo, hi, kb, [A sf tensors], [B sf tensors], s_a, s_b)
-    for bi, (lo, hi) in enumerate(_blocks(k, cfg.k_block)):
+    blocks = []  # per block: (lo, hi, kb, [A sf tensors], [B sf tensors], s_a, s_b, [A flags], [B flags])
+    for bi, (lo, hi) in enumerate(kblocks):
         kb = hi - lo
         params = compute_params(53, cfg.type2.mant_bits, cfg.type3.mant_bits, kb)
         if not params.feasible:
@@ -241,6 +246,7 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
         mp, np_ = _panel_plan(m, n, kb, eb, torch) if m and n else (max(m, 1), max(n, 1))
         s_a = s_b = 0
         sfa, sfb = [], []
+        hfa, hfb = [], []  # non-deferred: host flag words of the splits
         for j0 in range(0, max(n, 1), np_):
             j1 = min(n, j0 + np_)
             for i0 in range(0, max(m, 1), mp):
@@ -259,13 +265,15 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
                         sfb.append(sb.sf)
                     s_dev = torch.cat([sa.sf[:1], sb.sf[:1]])
                 else:
-                    fo = None if cfg.type2.name in _FP6 else flags  # FP6: raise split errors right away
+                    eager = cfg.type2.name in _FP6  # FP6: raise split errors (SlicingInfeasible) right away
                     if i0 == 0:
                         Bt = transpose_device(B[lo:hi, j0:j1])
                         (sa, sb), _ = split_many_device([A[i0:i1, lo:hi], Bt], cfg.type2, params, emu,
-                                                        flags_out=fo)
+                                                        check=eager)
+                        hfb.append(sb.host_flags)
                     else:
-                        (sa,), _ = split_many_device([A[i0:i1, lo:hi]], cfg.type2, params, emu, flags_out=fo)
+                        (sa,), _ = split_many_device([A[i0:i1, lo:hi]], cfg.type2, params, emu, check=eager)
+                    hfa.append(sa.host_flags)
                     s_a, s_b = max(s_a, sa.s), max(s_b, sb.s)
                     s_dev = None
                 if timing:
@@ -275,24 +283,24 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
                 if host_out is not None and last and mp == m and np_ == n:
                     host = (host_out, _copy_stream(torch).cuda_stream)
                 _pair_pass(torch, cfg, sa, sb, i1 - i0, j1 - j0, kb, order, cutoff, emu, bi, C, i0, j0, n,
-                           flags, sp, host, s_dev)
+                           gflags[bi:bi + 1], sp, host, s_dev)
                 if timing:
                     ev[2].record()
                     evs.append(ev)
             del Bt, sb
-        blocks.append((lo, hi, kb, sfa, sfb, s_a, s_b))
+        blocks.append((lo, hi, kb, sfa, sfb, s_a, s_b, hfa, hfb))
     if host_out is not None:
         if mp == m and np_ == n and m and n:
             _copy_stream(torch).synchronize()
         else:  # panelled: plain copy after the last panel
             host_out.copy_(C)
     # The one synchronisation: split counts / flags (deferred mode) + GEMM flags.
-    words = [flags] + [t for b in blocks for t in b[3] + b[4]]
+    words = [gflags] + [t for b in blocks for t in b[3] + b[4]]
     host = torch.cat(words).cpu().tolist()
-    gemm_flags, pos = host[0] & 0xFFFFFFFF, 1
+    gemm_flags, pos = [v & 0xFFFFFFFF for v in host[:gflags.numel()]], gflags.numel()
     split_words = []
-    for lo, hi, kb, sfa, sfb, s_a, s_b in blocks:
-        fa, fb = [], []
+    for lo, hi, kb, sfa, sfb, s_a, s_b, hfa, hfb in blocks:
+        fa, fb = list(hfa), list(hfb)
         for _ in sfa:
             s_a = max(s_a, host[pos])
             fa.append(host[pos + 1] & 0xFFFFFFFF)
@@ -313,10 +321,10 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
         stats.accum_ops += 2 * m * n * kept + m * n
     if any(f & _lib.FLAG_PLANE_CAP for fa, fb in split_words for f in fa + fb):
         return oz_gemm_device(A, B, cfg, out=C, timing=timing, host_out=host_out, deferred=False)
-    for fa, fb in split_words:  # reference order: block by block, A before B
+    for bi, (fa, fb) in enumerate(split_words):  # reference order: block by block, A, B, then terms
         for f in fa + fb:
             _lib.raise_for_flags(f, "split")
-    _lib.raise_for_flags(gemm_flags, "pair gemm")
+        _lib.raise_for_flags(gemm_flags[bi], "pair gemm")
     if timing:
         stats.t_slice = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3
         stats.t_gemm = sum(e[1].elapsed_time(e[2]) for e in evs) / 1e3

@@ -115,6 +115,7 @@ class DeviceSlices:
     ld: int
     fmt: FormatSpec
     sf: object = None
+    host_flags: int = 0  # split_many_device: this matrix's flag word (read at its sync)
 
     def codes(self):
         """Codes as a [s, rows, kb] uint8/uint16 torch tensor view."""
@@ -247,9 +248,13 @@ def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, str
                 _lib.call("oz_split_rows", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu), s_max,
                           planes.data_ptr(), ld, expo.data_ptr(), row_cnt.data_ptr(),
                           (flags_out if flags_out is not None else fw).data_ptr(), sp)
-                if check and flags_out is None:
-                    _lib.raise_for_flags(int(fw.item()) & 0xFFFFFFFF, "split")
+                if flags_out is None:
+                    flags |= int(fw.item()) & 0xFFFFFFFF  # representability (write pass only)
+                    if check:
+                        _lib.raise_for_flags(flags, "split")
+            full = flags
         else:
+            full = flags
             rep = flags & _lib.FLAG_NOT_REPRESENTABLE
             flags &= ~_lib.FLAG_NOT_REPRESENTABLE
             if check:
@@ -264,7 +269,7 @@ def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, str
                 _lib.call("oz_split_pad", planes.data_ptr(), ld, rows, code, s_max, expo.data_ptr(),
                           row_cnt.data_ptr(), None, sp)
         all_flags |= flags
-        out.append(DeviceSlices(planes, expo, row_cnt[:rows], s_max, rows, kb, ld, fmt))
+        out.append(DeviceSlices(planes, expo, row_cnt[:rows], s_max, rows, kb, ld, fmt, host_flags=full))
     return out, all_flags
 
 

@@ -31,3 +31,12 @@ def cuda():
 
     __graft_entry__.build()
     return torch
+
+
+@pytest.fixture
+def pair_variant(cuda):
+    """Force oz_pair_gemm's kernel variant for one test, then restore automatic."""
+    from paper_2508_00441_b200 import _lib
+
+    yield _lib.set_pair_variant
+    _lib.set_pair_variant(0, 0, 0)

@@ -190,10 +190,34 @@ def gen_emu():
                         rr=fp64emu.add_arrays(ra, rb).view(np.uint64))
 
 
+def gen_errors_ext():
+    """errors_ext.json: what the reference raises (class name) or returns
+    (sha256 of the C bits) for every case in error_cases.py."""
+    import hashlib
+
+    sys.path.insert(0, str(HERE))
+    from error_cases import cases
+
+    out = {}
+    for name, (A, B, kw) in cases().items():
+        kw = dict(kw)
+        cfg = R.GemmConfig(R.get_format(kw.pop("type2")), R.get_format(kw.pop("type3")), **kw)
+        try:
+            C = R.oz_gemm(A, B, cfg).C
+            out[name] = ["ok", hashlib.sha256(np.ascontiguousarray(C).view(np.uint64).tobytes()).hexdigest()]
+        except Exception as e:  # noqa: BLE001
+            out[name] = ["raise", type(e).__name__]
+    (HERE / "errors_ext.json").write_text(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["errors_ext"]:
+        gen_errors_ext()
+        raise SystemExit
     gen_params()
     gen_slices()
     gen_gemm()
     gen_errors()
     gen_emu()
+    gen_errors_ext()
     print("golden fixtures written to", HERE)

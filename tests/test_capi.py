@@ -81,13 +81,31 @@ def _sass_of(lib_path, kernel_substr):
 FP64_OPS = re.compile(r"\b(DFMA|DADD|DMUL|DSETP|DMNMX|DSET|F2F\.F64|F2F\.F32\.F64|I2F\.F64|F2I\.F64|DRCP|DMMA)\b")
 
 
+# Every kernel an emulated-FP64 oz_gemm launches (fp64_emulation=True): the
+# split_fused_kernel<threads, EPT, cluster, elem_bytes, emu=true> instantiations,
+# pair_gemm_kernel<emu=true, ...>, and the mode-independent helpers (code table,
+# zero padding, transpose, B-exponent prep, tile counts).
+EMU_SPLIT = re.compile(r"split_fused_kernelILi\d+ELi\d+ELi\d+ELi\d+ELb1EE")
+EMU_HELPERS = ("build_code_table_kernel", "pad_planes_kernel", "transpose_kernel", "prep_eb_kernel",
+               "tile_counts_kernel")
+
+
+def is_emulated_path_kernel(name: str) -> bool:
+    return ("pair_gemm_kernelILb1E" in name or EMU_SPLIT.search(name) is not None
+            or any(h in name for h in EMU_HELPERS))
+
+
 def test_emulated_kernels_have_no_fp64_arithmetic(lib):
+    """north_star: the emulated path contains no DFMA/DADD/DMUL (or any other
+    FP64 instruction) in its SASS — checked over all 20 emulated split / pair-GEMM
+    instantiations and the 5 helpers they run with."""
     from paper_2508_00441_b200 import _lib
 
-    # pair_gemm_kernel<true> -> _ZN2oz16pair_gemm_kernelILb1EE... ; split_rows_kernel<E, W, true>
-    sel = _sass_of(_lib.LIB_PATH, lambda k: ("pair_gemm_kernelILb1E" in k) or
-                   (re.search(r"split_rows_kernelILi\d+ELb[01]ELb1E", k) is not None))
-    assert len(sel) >= 3
+    sel = _sass_of(_lib.LIB_PATH, is_emulated_path_kernel)
+    n_split = sum(1 for k in sel if EMU_SPLIT.search(k))
+    n_pair = sum(1 for k in sel if "pair_gemm_kernelILb1E" in k)
+    assert n_split == 16 and n_pair == 4, (n_split, n_pair)
+    assert all(any(h in k for k in sel) for h in EMU_HELPERS)
     for name, lines in sel.items():
         bad = [ln for ln in lines if FP64_OPS.search(ln)]
         assert not bad, f"{name} contains FP64 arithmetic: {bad[:3]}"

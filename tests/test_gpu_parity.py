@@ -71,12 +71,10 @@ CASES = [
                                              f"-ms{c[8]}-{c[9][:5]}-cut{c[10]}" for c in CASES])
 @pytest.mark.parametrize("skip", [True, False])
 @pytest.mark.parametrize("variant", [("1", "128"), ("2", "128"), ("2", "192")], ids=lambda v: f"cta{v[0]}-n{v[1]}")
-def test_oz_gemm_bitwise(cuda, case, skip, variant, monkeypatch):
+def test_oz_gemm_bitwise(cuda, case, skip, variant, pair_variant):
     import oracle
 
-    # kernel variant, read by oz_pair_gemm at each launch
-    monkeypatch.setenv("OZ_CTA_GROUP", variant[0])
-    monkeypatch.setenv("OZ_TILE_N", variant[1])
+    pair_variant(int(variant[0]), int(variant[1]))  # kernel variant of oz_pair_gemm
 
     oz = _oz()
     m, n, k, phi, t2, t3, kbk, emu, ms, order, cut = case

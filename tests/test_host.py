@@ -206,3 +206,31 @@ def test_fp6_pack_unpack_roundtrip():
     one[0, 10] = 63
     v = int.from_bytes(_pack_fp6(one)[0].tobytes(), "little")
     assert v == 63 << 60
+
+
+def test_lp_gemm_refuses_products_whose_accumulation_can_round():
+    """lp_gemm is the exact-product seam: operands whose per-step type3
+    accumulation could round (lpgemm.py:49-77) raise instead of returning an
+    FP32-accumulated result that could differ from the reference."""
+    from paper_2508_00441_b200 import LpMatrix, get_format, lp_gemm
+    from paper_2508_00441_b200.lpgemm import accumulation_is_exact
+
+    f16, f32, e4m3 = get_format("fp16"), get_format("fp32"), get_format("fp8e4m3")
+    A = np.array([[1.0, 2.0 ** -13]])
+    B = np.array([[1.0], [1.0]])
+    assert accumulation_is_exact(A, B, f32) and not accumulation_is_exact(A, B, f16)
+    with pytest.raises(NotImplementedError):
+        lp_gemm(LpMatrix(A, f16), LpMatrix(B, f16), f16)
+    # 2^-12 * 2^-12 products next to 1.0: 25 bits, too wide for FP32
+    A = np.array([[1.0, 2.0 ** -12]])
+    B = np.array([[1.0], [2.0 ** -12]])
+    assert not accumulation_is_exact(A, B, f32)
+    with pytest.raises(NotImplementedError):
+        lp_gemm(LpMatrix(A, f16), LpMatrix(B, f16), f32)
+    # slice-like operands on the 2^-4 grid, k = 4096: exact
+    rng = np.random.default_rng(0)
+    A = rng.integers(-16, 17, size=(3, 4096)) / 16.0
+    B = rng.integers(-16, 17, size=(4096, 2)) / 16.0
+    assert accumulation_is_exact(A, B, f32)
+    assert not accumulation_is_exact(A * 1024, B * 1024, get_format("fp16"))
+    assert accumulation_is_exact(np.zeros((2, 2)), B[:2], e4m3)

@@ -72,3 +72,36 @@ def test_oracle_emu_equals_hw():
     C1, _ = oracle.oz_gemm(A, B, emu=False)
     C2, _ = oracle.oz_gemm(A, B, emu=True)
     assert np.array_equal(C1.view(np.uint64), C2.view(np.uint64))
+
+
+def test_oracle_config1_matches_reference():
+    """BASELINE config 1 (n = 1024, phi = 0.5, reference defaults): the oracle's
+    C has the sha256 of the C ozdgemm itself computed (gen_big_golden.py)."""
+    import hashlib
+
+    g = json.loads((GOLD / "config1.json").read_text())
+    n, phi = g["n"], g["phi"]
+    rng = np.random.default_rng(g["seed"])
+    A = (rng.random((n, n)) - 0.5) * np.exp(phi * rng.standard_normal((n, n)))
+    B = (rng.random((n, n)) - 0.5) * np.exp(phi * rng.standard_normal((n, n)))
+    C, info = oracle.oz_gemm(A, B, g["type2"], g["type3"])
+    assert info["flags"] == 0 and [list(b) for b in info["blocks"]] == g["blocks"]
+    assert hashlib.sha256(C.view(np.uint64).tobytes()).hexdigest() == g["sha256_C"]
+
+
+@pytest.mark.parametrize("key", ["64_1", "64_2", "64_3", "256_1", "512_2"])
+def test_dd_checker_matches_reference_ref_gemm(key):
+    """The double-double checker used for acceptance criteria 6/7 equals the
+    reference's exact ref_gemm bit for bit on the criteria's inputs, and the
+    naive restatement reproduces naive_gemm_fp64's error (golden accept.json)."""
+    import hashlib
+
+    meta = json.loads((GOLD / "accept.json").read_text())
+    n, seed = (int(v) for v in key.split("_"))
+    rng = np.random.default_rng(seed)
+    A = 1.0 + 9.0 * rng.random((n, n))
+    B = 1.0 + 9.0 * rng.random((n, n))
+    C = oracle.dd_gemm(A, B)
+    assert hashlib.sha256(C.view(np.uint64).tobytes()).hexdigest() == meta["hashes"][key]
+    err = float(np.max(np.abs(oracle.naive_gemm(A, B) - C) / np.abs(C)))
+    assert err == meta["err_naive"][key]
