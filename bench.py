@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--max-slices", type=int, default=None)
     ap.add_argument("--pair-cutoff", type=int, default=None)
     ap.add_argument("--skip-zero-pairs", action="store_true", help="enable (result-neutral) zero-pair skipping")
+    ap.add_argument("--slice-exponents", choices=("adaptive", "fixed"), default="adaptive",
+                    help="fixed: opt-in fixed-step slices + level-grouped accumulation (not bitwise the reference)")
     ap.add_argument("--no-extras", action="store_true", help="skip accuracy / cuBLAS / CPU-baseline legs")
     ap.add_argument("--cpu-rows", type=int, default=128, help="CPU-baseline sample: rows of C")
     ap.add_argument("--cpu-cols", type=int, default=1024, help="CPU-baseline sample: cols of C")
@@ -241,11 +243,14 @@ def workload_config(args, per_gpu=False):
         opts.append(f"pair_cutoff={args.pair_cutoff}")
     if args.kblock:
         opts.append(f"k_block={args.kblock}")
+    if args.slice_exponents != "adaptive":
+        opts.append(f"slice_exponents={args.slice_exponents}")
     return {"workload": f"Ozaki-{args.type2} DGEMM m=n=k={args.n} phi={args.phi} "
                         + (", ".join(opts) if opts else "reference defaults (all pairs, smallest-first, HW FP64)"),
             "m": args.n, "n": args.n, "k": args.n, "phi": args.phi, "type2": args.type2, "type3": args.type3,
             "k_block": args.kblock, "fp64_emulation": args.emu, "max_slices": args.max_slices,
-            "pair_cutoff": args.pair_cutoff, "skip_zero_pairs": args.skip_zero_pairs, "pace_slack": oz_pace_slack(),
+            "pair_cutoff": args.pair_cutoff, "skip_zero_pairs": args.skip_zero_pairs,
+            "slice_exponents": args.slice_exponents, "pace_slack": oz_pace_slack(),
             "l2": "inputs (2 x 512 MiB at n=8192) exceed the 126 MB L2; no flush",
             "parallelism": "2-D C tiles" if args.gpus > 1 else "1 GPU"}
 
@@ -279,7 +284,7 @@ def main():
     n = args.n
     cfg = oz.GemmConfig(oz.get_format(args.type2), oz.get_format(args.type3), k_block=args.kblock,
                         fp64_emulation=args.emu, max_slices=args.max_slices, pair_cutoff=args.pair_cutoff,
-                        skip_zero_pairs=args.skip_zero_pairs)
+                        skip_zero_pairs=args.skip_zero_pairs, slice_exponents=args.slice_exponents)
 
     # ---- inputs: this rank's C tile is n x n; A row-panel n x n, B column-panel n x n ----
     from paper_2508_00441_b200.distributed import TileGrid
@@ -363,7 +368,7 @@ def main():
 
     extras = {}
     if rank == 0 and not args.no_extras:
-        extras = run_extras(args, torch, oz, A, B, cfg, dev, world, Cbuf)
+        extras = run_extras(args, torch, oz, A, B, cfg, dev, world, Cbuf, st)
     # ---- e2e through the public API with host buffers (pinned) ----
     Ah = A.cpu().pin_memory()
     Bh = B.cpu().pin_memory()
@@ -409,7 +414,7 @@ def fp64_level_summary(extras):
     bound = acc["max_rel_err_cublas_dgemm"]
     cands = [("reference defaults", None, acc["max_rel_err_ozaki"])]
     for name, v in (var or {}).items():
-        if name.startswith("fp8_pair_cutoff_") and "max_rel_err" in v:
+        if (name.startswith("fp8_pair_cutoff_") or name.startswith("fp8_fixed_")) and "max_rel_err" in v:
             cands.append((name, v["tflops"], v["max_rel_err"]))
     ok = [c for c in cands if c[2] <= bound and c[1] is not None]
     if not ok:
@@ -420,7 +425,7 @@ def fp64_level_summary(extras):
             "vs_native_dgemm": tf / nat["tflops"]}
 
 
-def run_extras(args, torch, oz, A, B, cfg, dev, world=1, C_gpu=None):
+def run_extras(args, torch, oz, A, B, cfg, dev, world=1, C_gpu=None, st_gpu=None):
     """Accuracy vs the DD oracle, native cuBLAS DGEMM / FP8 on the same GPU,
     and the CPU baseline + bitwise parity sample (rank 0, N=1 leg)."""
     from paper_2508_00441_b200 import _lib
@@ -438,6 +443,12 @@ def run_extras(args, torch, oz, A, B, cfg, dev, world=1, C_gpu=None):
         Bs = B.index_select(1, ci).cpu().numpy()
         Cs = C_gpu.index_select(0, ri).index_select(1, ci).cpu().numpy()
         cb, Cref = cpu_baseline(args, len(rows), len(cols), n, A=As, B=Bs)
+        if args.slice_exponents == "fixed":  # opt-in mode: its own CPU restatement is the parity checker
+            import oracle
+
+            Cref, _ = oracle.oz_gemm_fixed(As, Bs, args.type2, args.type3, args.kblock, args.max_slices,
+                                           "smallest-first", args.pair_cutoff,
+                                           pad_to=[(b.s_x, b.s_y) for b in st_gpu.blocks])
         nbad = int(np.sum(Cs.view(np.uint64) != Cref.view(np.uint64)))
         out["parity"] = {"sample": f"C[{len(rows)}x{len(cols)}] of the timed run's C: rows in 4 runs, columns in 8 "
                                    f"runs spread over all tile waves; oracle on the same A rows / B columns",
@@ -545,6 +556,11 @@ def run_variants(args, torch, oz, A, B, Cdd, d, nz, c_cublas, dev, steps=3):
     out = {}
     for cut in (12, 11, 10):
         one(f"fp8_pair_cutoff_{cut}", oz.GemmConfig(f8, f32, pair_cutoff=cut), A, B, d, nz)
+    # opt-in fast mode: fixed-step slice exponents, level-grouped exact accumulation
+    for cut in (12, 11, 10):
+        one(f"fp8_fixed_cutoff_{cut}", oz.GemmConfig(f8, f32, pair_cutoff=cut, slice_exponents="fixed"), A, B, d, nz)
+    one("fp8_fixed_emulated_fp64_cutoff_11",
+        oz.GemmConfig(f8, f32, pair_cutoff=11, slice_exponents="fixed", fp64_emulation=True), A, B, d, nz)
     one("fp8_emulated_fp64", oz.GemmConfig(f8, f32, fp64_emulation=True), A, B, d, nz)
     one("fp16_kblock1024_phi0.5", oz.GemmConfig(f16, f32, k_block=1024), A, B, d, nz)
     one("fp6e3m2", oz.GemmConfig(oz.get_format("fp6e3m2"), f32), A, B, d, nz)
@@ -559,6 +575,8 @@ def run_variants(args, torch, oz, A, B, Cdd, d, nz, c_cublas, dev, steps=3):
     one("fp16_kblock1024_phi4", oz.GemmConfig(f16, f32, k_block=1024), A4, B4, d4, nz4, cub4)
     one("fp8_phi4", oz.GemmConfig(f8, f32), A4, B4, d4, nz4, cub4)
     one("fp8_phi4_pair_cutoff_12", oz.GemmConfig(f8, f32, pair_cutoff=12), A4, B4, d4, nz4, cub4)
+    one("fp8_phi4_fixed_cutoff_12", oz.GemmConfig(f8, f32, pair_cutoff=12, slice_exponents="fixed"), A4, B4, d4, nz4,
+        cub4)
     del A4, B4, Cdd4
     return out
 

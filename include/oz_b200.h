@@ -66,11 +66,26 @@ int oz_split_fused(const double* X, int64_t rows, int64_t kb, int64_t ldx, int t
                    void* coeff, int64_t ld_coeff, int32_t* expo, int32_t* row_cnt, int32_t* s_max, uint32_t* flags,
                    void* stream);
 
+/* Fixed-step variant of oz_split_fused (opt-in extension, no reference
+ * counterpart; GemmConfig.slice_exponents = "fixed"): slice p of a row gets the
+ * exponent c_p = c_0 - p (54 - rho), c_0 = ceil_log2 max|x| as in the reference,
+ * instead of ceil_log2 of the residual's max (slicing.py:145-152).  The reference's
+ * RN residual bound |x - v| <= 2^(c_p + rho - 54) keeps every coefficient within
+ * |k| <= 2^(53 - rho), so the slices are exact and error-free exactly as before;
+ * what changes is that all pairs with equal p + q share one scale.  Exponents are
+ * written for all `cap` planes (the sequence continues through padding planes; pad
+ * with oz_split_pad(..., expo = NULL, ...)).  max_planes > 0 stops each row after
+ * that many slices (planes past a pair cutoff are never used). */
+int oz_split_fixed(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2, int rho, int emu, int cap,
+                   int max_planes, void* coeff, int64_t ld_coeff, int32_t* expo, int32_t* row_cnt, int32_t* s_max,
+                   uint32_t* flags, void* stream);
+
 /* Zero slices for rows exhausted before the global s (slicing.py:149-152): for
  * every row r, planes [row_cnt[r], s) of coeff[.][rows][ld_coeff] are zeroed and
  * their exponents set to 0.  Completes oz_split_fused.  s_dev (nullable): read s
  * from device memory (oz_split_fused's s_max word) instead, capped at `s` (the
- * planes allocated) — no host round trip. */
+ * planes allocated) — no host round trip.  expo == NULL leaves the exponents
+ * untouched (fixed-step planes, oz_split_fixed). */
 int oz_split_pad(void* coeff, int64_t ld_coeff, int64_t rows, int type2, int s, int32_t* expo,
                  const int32_t* row_cnt, const int32_t* s_dev, void* stream);
 
@@ -133,6 +148,19 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
                  int order, int pair_cutoff, int emu, int accumulate, double* C, int64_t ldc, uint32_t* flags,
                  void* workspace, int64_t workspace_bytes, int pace_slack, double* C_host, int64_t ldc_host,
                  void* copy_stream, const int32_t* s_dev, void* stream);
+
+/* oz_pair_gemm for fixed-step slices (oz_split_fixed; opt-in extension): up to
+ * group_max consecutive pairs of one anti-diagonal p + q = l (they share the scale
+ * 2^(c0A + c0B - l (54 - rho))) accumulate in one TMEM accumulator — exact while
+ * group_max * kb * 2^(2 (53 - rho)) <= 2^24 — and the FP64 epilogue (hardware or
+ * emulated) adds each group once, in the pair order's group sequence.  No
+ * zero-pair skipping.  Other arguments as oz_pair_gemm. */
+int oz_pair_gemm_grouped(const void* a_planes, const void* b_planes, int64_t ld_a, int64_t ld_b, int planes_a,
+                         int planes_b, const int32_t* expo_a, const int32_t* expo_b, int64_t m, int64_t n,
+                         int64_t kb, int sx, int sy, int type2, int order, int pair_cutoff, int group_max, int emu,
+                         int accumulate, double* C, int64_t ldc, uint32_t* flags, void* workspace,
+                         int64_t workspace_bytes, int pace_slack, double* C_host, int64_t ldc_host,
+                         void* copy_stream, const int32_t* s_dev, void* stream);
 
 /* Bytes of device workspace oz_pair_gemm needs for these sizes (0 if there is
  * nothing to compute). */

@@ -163,3 +163,90 @@ def naive_gemm(A, B):
     for t in range(A.shape[1]):
         C += A[:, t, None] * B[t, None, :]
     return C
+
+
+def split_rows_fixed(X, rho: int, max_planes: int = 0):
+    """Fixed-step slicing (the opt-in ``slice_exponents="fixed"`` extension; no
+    reference counterpart): the reference's _slice_rows iteration
+    (slicing.py:144-176) with c_p = c_0 - p (54 - rho), c_0 = ceil_log2 max|x|.
+    Returns (coeff [s, rows, kb], expo [s, rows], counts, s)."""
+    X = np.array(X, dtype=np.float64)
+    rows, kb = X.shape
+    w = 54 - rho
+    mx = np.max(np.abs(X), axis=1) if kb else np.zeros(rows)
+    m, e = np.frexp(np.where(mx > 0, mx, 1.0))
+    c0 = np.where(mx > 0, np.where(m == 0.5, e - 1, e), 0).astype(np.int64)
+    coeffs, cnt, p = [], np.zeros(rows, dtype=np.int64), 0
+    while np.any(X != 0) and (max_planes <= 0 or p < max_planes):
+        active = np.any(X != 0, axis=1)
+        c = c0 - p * w
+        sigma = np.ldexp(1.5, c + rho - 1)[:, None]
+        v = (X + sigma) - sigma
+        v[~active] = 0.0
+        X = X - v
+        coeffs.append(np.ldexp(v, -c[:, None]))
+        cnt[active] = p + 1
+        p += 1
+    s = len(coeffs)
+    expo = np.stack([c0 - q * w for q in range(s)]) if s else np.zeros((0, rows), dtype=np.int64)
+    coeff = np.stack(coeffs) if s else np.zeros((0, rows, kb))
+    return coeff, expo, cnt, s
+
+
+def oz_gemm_fixed(A, B, type2: str = "fp8e4m3", type3: str = "fp32", k_block: int = 0, max_slices=None,
+                  order: str = "smallest-first", pair_cutoff=None, pad_to=None):
+    """CPU restatement of the fixed-step, level-grouped pipeline
+    (GemmConfig.slice_exponents="fixed"): per block, pairs in the reference order
+    (ozgemm.py:179-183, restricted to p+q <= pair_cutoff), consecutive pairs of one
+    anti-diagonal summed exactly in groups of at most group_max, each group added
+    to Cb once as G * 2^(cA_p0 + cB_q0) with one RNE rounding, then C += Cb.
+    ``pad_to`` = [(s_A, s_B)] per block: extend the slices with zero planes
+    (continuing exponents) to those counts — a row/column sample of a larger
+    problem then walks the same pair groups as the full problem.
+    Returns (C, blocks [(lo, hi, sx, sy)])."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    B = np.ascontiguousarray(B, dtype=np.float64)
+    m, k = A.shape
+    n = B.shape[1]
+    m2, m3 = FMT_MANT[type2], FMT_MANT[type3]
+    blocks = [(0, k)] if k_block == 0 else [(lo, min(lo + k_block, k)) for lo in range(0, k, k_block)]
+    C = np.zeros((m, n))
+    info = []
+    for bi, (lo, hi) in enumerate(blocks):
+        kb = hi - lo
+        rho, _ = compute_rho(53, m2, m3, kb)
+        lim = [v for v in (max_slices, None if pair_cutoff is None else pair_cutoff + 1) if v]
+        mp = min(lim) if lim else 0
+        ca, ea, _, sa = split_rows_fixed(A[:, lo:hi], rho, mp)
+        cbt, eb, _, sb = split_rows_fixed(B[lo:hi, :].T, rho, mp)
+        if pad_to is not None:
+            w = 54 - rho
+
+            def pad(c, e, s, want):
+                if want <= s:
+                    return c, e, s
+                c = np.concatenate([c, np.zeros((want - s,) + c.shape[1:])])
+                e0 = e[0] if s else np.zeros(c.shape[1], dtype=np.int64)
+                return c, np.stack([e0 - q * w for q in range(want)]), want
+
+            ca, ea, sa = pad(ca, ea, sa, pad_to[bi][0])
+            cbt, eb, sb = pad(cbt, eb, sb, pad_to[bi][1])
+        sx, sy = min(sa, max_slices or sa), min(sb, max_slices or sb)
+        info.append((lo, hi, sx, sy))
+        gmax = max(1, min(64, (1 << (24 - 2 * (53 - rho))) // kb))
+        pairs = [(p, q) for p in range(sx) for q in range(sy) if pair_cutoff is None or p + q <= pair_cutoff]
+        sgn = -1 if order == "smallest-first" else 1
+        pairs.sort(key=lambda pq: (sgn * (pq[0] + pq[1]), pq[0], pq[1]))
+        Cb = np.zeros((m, n))
+        i = 0
+        while i < len(pairs):
+            p0, q0 = pairs[i]
+            G = np.zeros((m, n))
+            j = i
+            while j < len(pairs) and j - i < gmax and sum(pairs[j]) == p0 + q0:
+                G += ca[pairs[j][0]] @ cbt[pairs[j][1]].T  # exact: small multiples of the slice grid
+                j += 1
+            Cb = Cb + np.ldexp(G, ea[p0][:, None] + eb[q0][None, :])
+            i = j
+        C = Cb.copy() if bi == 0 else C + Cb
+    return C, info

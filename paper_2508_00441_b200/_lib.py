@@ -38,6 +38,7 @@ _I64 = ctypes.c_int64
 _I = ctypes.c_int
 SIGNATURES = {
     "oz_split_fused": (_I, [_P, _I64, _I64, _I64, _I, _I, _I, _I, _P, _I64, _P, _P, _P, _P, _P]),
+    "oz_split_fixed": (_I, [_P, _I64, _I64, _I64, _I, _I, _I, _I, _I, _P, _I64, _P, _P, _P, _P, _P]),
     "oz_split_pad": (_I, [_P, _I64, _I64, _I, _I, _P, _P, _P, _P]),
     "oz_split_count": (_I, [_P, _I64, _I64, _I64, _I, _I, _I, _P, _P, _P, _P]),
     "oz_split_rows": (_I, [_P, _I64, _I64, _I64, _I, _I, _I, _I, _P, _I64, _P, _P, _P, _P]),
@@ -45,6 +46,8 @@ SIGNATURES = {
     "oz_tile_counts": (_I, [_P, _I64, _P, _P]),
     "oz_pair_gemm": (_I, [_P, _P, _I64, _I64, _I, _I, _P, _P, _P, _P, _I64, _I64, _I64, _I, _I, _I,
                           _I, _I, _I, _I, _P, _I64, _P, _P, _I64, _I, _P, _I64, _P, _P, _P]),
+    "oz_pair_gemm_grouped": (_I, [_P, _P, _I64, _I64, _I, _I, _P, _P, _I64, _I64, _I64, _I, _I, _I, _I, _I, _I, _I,
+                                  _I, _P, _I64, _P, _P, _I64, _I, _P, _I64, _P, _P, _P]),
     "oz_pair_gemm_workspace": (ctypes.c_int64, [_I64, _I64, _I, _I, _I]),
     "oz_set_pair_variant": (_I, [_I, _I, _I]),
     "oz_lp_gemm": (_I, [_P, _P, _I64, _I64, _I64, _I64, _I64, _I, _P, _I64, _P]),

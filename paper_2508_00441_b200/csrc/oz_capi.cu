@@ -286,6 +286,10 @@ __global__ void emu_add_batch_kernel(const uint64_t* __restrict__ a, const uint6
   if (f) atomicOr(flags, f);
 }
 
+int split_impl(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2, int rho, int emu, int cap,
+               int fixed_w, int max_planes, void* coeff, int64_t ld_coeff, int32_t* expo, int32_t* row_cnt,
+               int32_t* s_max, uint32_t* flags, void* stream);
+
 }  // namespace
 
 extern "C" {
@@ -300,6 +304,24 @@ int64_t oz_pair_gemm_workspace(int64_t m, int64_t n, int sx, int sy, int pair_cu
 int oz_split_fused(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2, int rho, int emu, int cap,
                    void* coeff, int64_t ld_coeff, int32_t* expo, int32_t* row_cnt, int32_t* s_max, uint32_t* flags,
                    void* stream) {
+  return split_impl(X, rows, kb, ldx, type2, rho, emu, cap, 0, 0, coeff, ld_coeff, expo, row_cnt, s_max, flags,
+                    stream);
+}
+
+int oz_split_fixed(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2, int rho, int emu, int cap,
+                   int max_planes, void* coeff, int64_t ld_coeff, int32_t* expo, int32_t* row_cnt, int32_t* s_max,
+                   uint32_t* flags, void* stream) {
+  if (rho < 42 || rho > 53 || max_planes < 0) return OZ_EINVAL;
+  return split_impl(X, rows, kb, ldx, type2, rho, emu, cap, 54 - rho, max_planes, coeff, ld_coeff, expo, row_cnt,
+                    s_max, flags, stream);
+}
+
+}  // extern "C"
+
+namespace {
+int split_impl(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2, int rho, int emu, int cap,
+               int fixed_w, int max_planes, void* coeff, int64_t ld_coeff, int32_t* expo, int32_t* row_cnt,
+               int32_t* s_max, uint32_t* flags, void* stream) {
   LpFormat f;
   uint32_t idf;
   if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
@@ -314,6 +336,7 @@ int oz_split_fused(const double* X, int64_t rows, int64_t kb, int64_t ldx, int t
   P.X = X; P.rows = rows; P.kb = kb; P.ldx = ldx; P.rho = rho; P.cap = cap;
   P.coeff = static_cast<uint8_t*>(coeff); P.ld = ld_coeff; P.expo = expo; P.row_cnt = row_cnt;
   P.s_max = s_max; P.flags = flags; P.kmax = 1 << (53 - rho);
+  P.fixed_w = fixed_w; P.max_planes = max_planes;
   P.pack6 = (type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3) ? 1 : 0;
   if (P.pack6 && (ld_coeff & 127)) return OZ_EINVAL;  // packed FP6 rows: multiples of 128 codes
   int rc = code_table(type2, f, rho, st, &P.table, &P.table_clean);
@@ -321,6 +344,9 @@ int oz_split_fused(const double* X, int64_t rows, int64_t kb, int64_t ldx, int t
   if (f.bytes == 1) return emu ? launch_fused_cfg<1, true>(P, st) : launch_fused_cfg<1, false>(P, st);
   return emu ? launch_fused_cfg<2, true>(P, st) : launch_fused_cfg<2, false>(P, st);
 }
+}  // namespace
+
+extern "C" {
 
 int oz_split_pad(void* coeff, int64_t ld_coeff, int64_t rows, int type2, int s, int32_t* expo,
                  const int32_t* row_cnt, const int32_t* s_dev, void* stream) {
@@ -329,7 +355,7 @@ int oz_split_pad(void* coeff, int64_t ld_coeff, int64_t rows, int type2, int s, 
   if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
   if (rows < 0 || s < 0 || (ld_coeff * f.bytes) % 16) return OZ_EINVAL;
   if (rows == 0 || s == 0) return OZ_OK;
-  if (!coeff || !expo || !row_cnt) return OZ_EINVAL;
+  if (!coeff || !row_cnt) return OZ_EINVAL;  // expo == NULL: exponents left as they are (fixed-step planes)
   const unsigned blocks = (unsigned)((rows + 7) / 8);
   const int64_t row_bytes = (type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3) ? ld_coeff * 3 / 4 : ld_coeff * f.bytes;
   oz::pad_planes_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<uint8_t*>(coeff), row_bytes,
@@ -408,12 +434,12 @@ int oz_tile_counts(const int32_t* row_cnt, int64_t rows, int32_t* tile_cnt, void
   return launch_status();
 }
 
-int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64_t ld_b, int planes_a,
-                 int planes_b, const int32_t* expo_a, const int32_t* expo_b, const int32_t* tile_cnt_a,
-                 const int32_t* tile_cnt_b, int64_t m, int64_t n, int64_t kb, int sx, int sy, int type2,
-                 int order, int pair_cutoff, int emu, int accumulate, double* C, int64_t ldc, uint32_t* flags,
-                 void* workspace, int64_t workspace_bytes, int pace_slack, double* C_host, int64_t ldc_host,
-                 void* copy_stream, const int32_t* s_dev, void* stream) {
+static int pair_gemm_impl(const void* a_planes, const void* b_planes, int64_t ld_a, int64_t ld_b, int planes_a,
+                          int planes_b, const int32_t* expo_a, const int32_t* expo_b, const int32_t* tile_cnt_a,
+                          const int32_t* tile_cnt_b, int64_t m, int64_t n, int64_t kb, int sx, int sy, int type2,
+                          int order, int pair_cutoff, int emu, int accumulate, double* C, int64_t ldc,
+                          uint32_t* flags, void* workspace, int64_t workspace_bytes, int pace_slack, double* C_host,
+                          int64_t ldc_host, void* copy_stream, const int32_t* s_dev, int group_max, void* stream) {
   LpFormat f;
   uint32_t idf;
   if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
@@ -449,11 +475,14 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
   if (!workspace || (size_t)workspace_bytes < pl.eb_bytes) return OZ_EINVAL;  // see oz_pair_gemm_workspace
   P.group = pl.group;
   P.hint_a = P.hint_b = oz::kEvictNormal;
-  // Non-zero G: FP32 exponent field in [127 - 2 m2, 127 + ceil(log2 kb)] (PairParams).
+  // Non-zero G (a sum of up to group_max pair products): FP32 exponent field in
+  // [127 - 2 m2, 127 + ceil(log2(group_max kb))] (PairParams).
+  if (group_max < 1 || group_max > 64) return OZ_EINVAL;
+  P.group_max = group_max;
   P.g_lo = 127 - 2 * (f.mbits + 1);
   {
     int lg = 0;
-    while ((1ll << lg) < kb) ++lg;
+    while ((1ll << lg) < kb * group_max) ++lg;
     P.g_hi = 127 + lg;
   }
   P.trace = nullptr; P.trace_cap = 0; P.debug = 0;
@@ -546,6 +575,28 @@ int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64
     }
   }
   return launch_status();
+}
+
+int oz_pair_gemm(const void* a_planes, const void* b_planes, int64_t ld_a, int64_t ld_b, int planes_a,
+                 int planes_b, const int32_t* expo_a, const int32_t* expo_b, const int32_t* tile_cnt_a,
+                 const int32_t* tile_cnt_b, int64_t m, int64_t n, int64_t kb, int sx, int sy, int type2,
+                 int order, int pair_cutoff, int emu, int accumulate, double* C, int64_t ldc, uint32_t* flags,
+                 void* workspace, int64_t workspace_bytes, int pace_slack, double* C_host, int64_t ldc_host,
+                 void* copy_stream, const int32_t* s_dev, void* stream) {
+  return pair_gemm_impl(a_planes, b_planes, ld_a, ld_b, planes_a, planes_b, expo_a, expo_b, tile_cnt_a, tile_cnt_b,
+                        m, n, kb, sx, sy, type2, order, pair_cutoff, emu, accumulate, C, ldc, flags, workspace,
+                        workspace_bytes, pace_slack, C_host, ldc_host, copy_stream, s_dev, 1, stream);
+}
+
+int oz_pair_gemm_grouped(const void* a_planes, const void* b_planes, int64_t ld_a, int64_t ld_b, int planes_a,
+                         int planes_b, const int32_t* expo_a, const int32_t* expo_b, int64_t m, int64_t n,
+                         int64_t kb, int sx, int sy, int type2, int order, int pair_cutoff, int group_max, int emu,
+                         int accumulate, double* C, int64_t ldc, uint32_t* flags, void* workspace,
+                         int64_t workspace_bytes, int pace_slack, double* C_host, int64_t ldc_host,
+                         void* copy_stream, const int32_t* s_dev, void* stream) {
+  return pair_gemm_impl(a_planes, b_planes, ld_a, ld_b, planes_a, planes_b, expo_a, expo_b, nullptr, nullptr, m, n,
+                        kb, sx, sy, type2, order, pair_cutoff, emu, accumulate, C, ldc, flags, workspace,
+                        workspace_bytes, pace_slack, C_host, ldc_host, copy_stream, s_dev, group_max, stream);
 }
 
 int oz_emu_add_batch(const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t n, int mode, uint32_t* flags,

@@ -115,6 +115,12 @@ struct PairParams {
   // [127 - 2 m2, 127 + ceil(log2 kb)].  The epilogue's fast (unchecked) term path is
   // taken only when every term of a (row, pair) is then provably normal.
   int g_lo, g_hi;
+  // Pairs summed in one TMEM accumulator before the epilogue (fixed-step slice
+  // exponents only, GemmConfig.slice_exponents="fixed"): consecutive pairs of one
+  // anti-diagonal p + q = l share the scale 2^(c0A + c0B - l w), so up to group_max
+  // of them accumulate exactly in FP32 (group_max * kb * 2^(2(53-rho)) <= 2^24) and
+  // the FP64 epilogue runs once per group.  1 = one pair per epilogue pass (reference).
+  int group_max;
   unsigned long long* trace; // diagnostics (OZ_DIAGNOSTICS builds only): per-pair timestamps of unit 0
   int trace_cap;             // entries (pairs) the trace holds
   // Diagnostics only (OZ_DIAGNOSTICS builds, OZ_DEBUG_MODE): bit 0 = epilogue skips the
@@ -626,7 +632,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
         tile_coords(tile, P.tiles_m, P.tiles_n, P.group, tm, tn);
         unit_limits<kCta, kN>(P, sx, sy, tm, tn, lp, lq);
         PairIter pi;
-        for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
+        pi.init(lp, lq, P.order, P.cutoff);
+        for (; pi.valid(); ++acc_it) {
           const uint32_t buf = acc_it % kAccBufs;
           const bool tr = OZ_DIAGNOSTICS && P.trace && unit == 0 && acc_it < (uint32_t)P.trace_cap;
           long long full_wait = 0;
@@ -635,23 +642,30 @@ __global__ void __launch_bounds__(kPThreads, 1)
           if (tr && lane == 0) P.trace[acc_it * 8 + 1] = clock64();
           tc_fence_after();
           const uint32_t d_tmem = tmem + buf * kN;
-          for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
-            const uint32_t st = it % kStages;
-            const long long tw0 = tr ? clock64() : 0;
-            mbar_wait(&s.full[st], (it / kStages) & 1);
-            if (tr) full_wait += clock64() - tw0;
-            tc_fence_after();
-            if (elect_one()) {
-              const uint64_t ad = smem_desc_sw128(s.a[st]), bd = smem_desc_sw128(s.b[st]);
+          // One accumulator per group of pairs (one pair unless group_max > 1).
+          const int lvl = pi.d;
+          int gcnt = 0;
+          do {
+            for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
+              const uint32_t st = it % kStages;
+              const long long tw0 = tr ? clock64() : 0;
+              mbar_wait(&s.full[st], (it / kStages) & 1);
+              if (tr) full_wait += clock64() - tw0;
+              tc_fence_after();
+              if (elect_one()) {
+                const uint64_t ad = smem_desc_sw128(s.a[st]), bd = smem_desc_sw128(s.b[st]);
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                const uint64_t off = (uint64_t)((kk * 32) >> 4);
-                mma_issue<kCta, kElemBytes>(d_tmem, ad + off, bd + off, idesc, (kbi | kk) != 0);
+                for (int kk = 0; kk < 4; ++kk) {
+                  const uint64_t off = (uint64_t)((kk * 32) >> 4);
+                  mma_issue<kCta, kElemBytes>(d_tmem, ad + off, bd + off, idesc, (gcnt | kbi | kk) != 0);
+                }
+                mma_commit_g<kCta>(&s.empty[st]);
               }
-              mma_commit_g<kCta>(&s.empty[st]);
+              __syncwarp();
             }
-            __syncwarp();
-          }
+            ++gcnt;
+            pi.next();
+          } while (pi.valid() && pi.d == lvl && gcnt < P.group_max);
           if (elect_one()) mma_commit_g<kCta>(&s.acc_full[buf]);
           if (tr && lane == 0) {
             P.trace[acc_it * 8 + 2] = clock64();
@@ -696,8 +710,20 @@ __global__ void __launch_bounds__(kPThreads, 1)
       }
 
       PairIter pi;
-      for (pi.init(lp_walk, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++acc_it) {
+      pi.init(lp_walk, lq, P.order, P.cutoff);
+      for (; pi.valid(); ++acc_it) {
+        // This accumulator holds the group starting at pair (p, q) (one pair unless
+        // group_max > 1; then its exponents give the whole level's scale, and a row
+        // whose slices p.. are all zero (p >= lp) contributes nothing).
         const int p = pi.p, q = pi.q();
+        {
+          const int lvl = pi.d;
+          int gcnt = 0;
+          do {
+            ++gcnt;
+            pi.next();
+          } while (pi.valid() && pi.d == lvl && gcnt < P.group_max);
+        }
         const uint32_t buf = acc_it % kAccBufs;
         const bool tr = OZ_DIAGNOSTICS && P.trace && unit == 0 && crank == 0 && warp == 4 && lane == 0 &&
                          acc_it < (uint32_t)P.trace_cap;

@@ -97,6 +97,15 @@ struct FusedSplitParams {
   int pack6;               // FP6: 16 codes -> 12 densely packed bytes (rows of ld*3/4 bytes),
                            // which TMA 16U6_ALIGN16B spreads to 16-byte groups in smem
   int table_clean;         // 1: no entry carries the not-representable bit
+  // Fixed-step exponents (opt-in extension, GemmConfig.slice_exponents="fixed"):
+  // fixed_w > 0 gives slice p the exponent c_p = c_0 - p * fixed_w (fixed_w = 54 - rho,
+  // the step the reference's RN residual bound guarantees) instead of ceil_log2 of the
+  // residual's max, so all pairs on an anti-diagonal p + q = l share one scale and
+  // can be summed exactly on the tensor cores.  Exponents are written for every
+  // allocated plane (padding planes keep the sequence).  max_planes > 0 stops after
+  // that many slices (pairs beyond a cutoff are never used).
+  int fixed_w;
+  int max_planes;
 };
 
 // table[k + K] = code of k * 2^(rho-53) (| 1<<16 if not representable).
@@ -321,6 +330,7 @@ __global__ void __launch_bounds__(kThreads, kThreads <= 256 ? 2 : 1) split_fused
   const uint32_t* tblc = tbl + K;
   const bool write = P.coeff != nullptr;  // count-only mode otherwise (no planes, no exponents)
   int cnt = 0;
+  int c_prev = 0;
   for (int it = 0;; ++it) {
     // Row max of the key: warp redux -> smem -> (cluster DSMEM).
     uint32_t m = __reduce_max_sync(0xFFFFFFFFu, key);
@@ -341,13 +351,15 @@ __global__ void __launch_bounds__(kThreads, kThreads <= 256 ? 2 : 1) split_fused
       flags |= FLAG_SLICE_CAP;
       break;
     }
+    if (P.max_planes > 0 && it >= P.max_planes) break;  // fixed mode: planes past the cutoff are unused
     if (write && it >= P.cap) {
       flags |= FLAG_PLANE_CAP_INTERNAL;
       break;
     }
     // c = ceil(log2 max|x|): exponent field = key >> 21, fraction non-zero = low 21 key bits.
     const int e = (int)(m >> 21) - 1023;
-    const int c = (m & 0x1FFFFFu) != 0 ? e + 1 : e;
+    const int c = (P.fixed_w > 0 && it > 0) ? c_prev - P.fixed_w : ((m & 0x1FFFFFu) != 0 ? e + 1 : e);
+    c_prev = c;
     const int sig_exp = c + P.rho - 1 + 1023;
     if (sig_exp < 1 || sig_exp > 2046) {
       flags |= FLAG_SIGMA_RANGE;
@@ -371,6 +383,10 @@ __global__ void __launch_bounds__(kThreads, kThreads <= 256 ? 2 : 1) split_fused
   if (t == 0 && rank == 0) {
     P.row_cnt[row] = cnt;
     atomicMax(P.s_max, cnt);
+    if (P.fixed_w > 0 && write) {  // the exponent sequence continues through the padding planes
+      const int c0 = cnt > 0 ? P.expo[row] : 0;
+      for (int p = cnt; p < P.cap; ++p) P.expo[(int64_t)p * P.rows + row] = c0 - p * P.fixed_w;
+    }
   }
   flags = __reduce_or_sync(0xFFFFFFFFu, flags);
   if (lane == 0 && flags) atomicOr(P.flags, flags);
@@ -389,7 +405,7 @@ __global__ void pad_planes_kernel(uint8_t* __restrict__ coeff, int64_t row_bytes
   for (int p = cnt; p < s; ++p) {
     uint4* dst = reinterpret_cast<uint4*>(coeff + ((int64_t)p * rows + row) * row_bytes);
     for (int64_t i = lane; i < row_bytes / 16; i += 32) dst[i] = make_uint4(0u, 0u, 0u, 0u);
-    if (lane == 0) expo[(int64_t)p * rows + row] = 0;
+    if (lane == 0 && expo) expo[(int64_t)p * rows + row] = 0;  // expo == nullptr: keep (fixed-step mode)
   }
 }
 

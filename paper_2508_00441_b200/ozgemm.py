@@ -10,9 +10,19 @@ order, bitwise the same C.  Per inner-product block [lo, hi)
   T = G*2^(eA+eB) and Cb += T in the epilogue,
   C = Cb (first block) / C + Cb                        -> oz_pair_gemm.cu (tensor-bound)
 
-Two opt-in extensions beyond the reference, both off by default:
+Opt-in extensions beyond the reference, all off by default:
   * ``pair_cutoff = d`` keeps only pairs with p + q <= d (a prefix-free subset
     of the reference order; ``d >= sx + sy - 2`` is exactly the reference);
+  * ``slice_exponents = "fixed"``: slice p of a row gets the exponent
+    c_p = c_0 - p (54 - rho) (c_0 as in the reference) instead of ceil_log2 of
+    the residual's max.  The slices stay exact (the reference's RN residual bound
+    is exactly this step), and every pair on an anti-diagonal p + q = l then has
+    the scale 2^(c0A + c0B - l (54 - rho)): up to ``group_max`` such pairs are
+    summed exactly in one FP32 tensor-core accumulator and the FP64 epilogue
+    runs once per group instead of once per pair.  C is then not bitwise the
+    reference's (fewer, differently placed roundings; accuracy vs a DD oracle
+    is measured in bench.py) — the fast FP64-level mode together with
+    ``pair_cutoff``;
   * ``skip_zero_pairs`` skips pairs whose A- or B-slice is all zero over a
     128x128 output tile: such a term is +0 and Cb is never -0, so C is bitwise
     unchanged (this is not an approximation).  Off by default: tiles then walk
@@ -39,6 +49,7 @@ __all__ = [
 ]
 
 _ACC_ORDERS = ("smallest-first", "largest-first")
+_EXP_MODES = ("adaptive", "fixed")
 
 # Cross-CTA pacing slack in pair-steps (scheduling only; 0 disables).
 PACE_SLACK = int(os.environ.get("OZ_PACE_SLACK", "2"))
@@ -58,6 +69,7 @@ class GemmConfig:
     # ---- extensions (defaults reproduce the reference bit for bit) ----
     pair_cutoff: int | None = None
     skip_zero_pairs: bool = False
+    slice_exponents: str = "adaptive"
 
     def __post_init__(self):
         if self.k_block < 0:
@@ -68,6 +80,8 @@ class GemmConfig:
             raise ValueError(f"accumulation_order must be one of {_ACC_ORDERS}")
         if self.pair_cutoff is not None and self.pair_cutoff < 0:
             raise ValueError("pair_cutoff must be >= 0")
+        if self.slice_exponents not in _EXP_MODES:
+            raise ValueError(f"slice_exponents must be one of {_EXP_MODES}")
 
 
 @dataclass
@@ -125,6 +139,14 @@ def pair_order(sx: int, sy: int, order: str = "smallest-first", cutoff: int | No
     else:
         pairs.sort(key=lambda pq: (pq[0] + pq[1], pq[0], pq[1]))
     return pairs
+
+
+def group_max(params, kb: int) -> int:
+    """Pairs of one anti-diagonal that one FP32 accumulator sums exactly
+    (fixed-step exponents): every product is a multiple of 2^(2(rho-53)) of
+    magnitude <= 1, so g pairs of depth kb stay exact while
+    g * kb * 2^(2(53-rho)) <= 2^24."""
+    return max(1, min(64, (1 << (24 - 2 * (53 - params.rho))) // kb))
 
 
 def _check_accumulator(params, kb: int):
@@ -225,6 +247,11 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
     emu = bool(cfg.fp64_emulation)
     order = 0 if cfg.accumulation_order == "smallest-first" else 1
     cutoff = -1 if cfg.pair_cutoff is None else int(cfg.pair_cutoff)
+    fixed = cfg.slice_exponents == "fixed"
+    # fixed-step slices past the pair limit are never used: stop the split there
+    lim = [v for v in (cfg.max_slices, None if cfg.pair_cutoff is None else cfg.pair_cutoff + 1) if v]
+    max_planes = min(lim) if fixed and lim else 0
+    fx = {"fixed": fixed, "max_planes": max_planes}
     stats = OzStats()
     C = out if out is not None else torch.empty((m, n), dtype=torch.float64, device=A.device)
     sp = _lib.stream_ptr(torch)
@@ -257,11 +284,11 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
                 # Row panel of A, column panel of B (columns as K-major rows); B's
                 # panel is sliced once per column panel (j0 loop outside).
                 if deferred:
-                    sa = split_deferred(A[i0:i1, lo:hi], cfg.type2, params, emu)
+                    sa = split_deferred(A[i0:i1, lo:hi], cfg.type2, params, emu, **fx)
                     sfa.append(sa.sf)
                     if i0 == 0:
                         Bt = transpose_device(B[lo:hi, j0:j1])
-                        sb = split_deferred(Bt, cfg.type2, params, emu)
+                        sb = split_deferred(Bt, cfg.type2, params, emu, **fx)
                         sfb.append(sb.sf)
                     s_dev = torch.cat([sa.sf[:1], sb.sf[:1]])
                 else:
@@ -269,10 +296,11 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
                     if i0 == 0:
                         Bt = transpose_device(B[lo:hi, j0:j1])
                         (sa, sb), _ = split_many_device([A[i0:i1, lo:hi], Bt], cfg.type2, params, emu,
-                                                        check=eager)
+                                                        check=eager, **fx)
                         hfb.append(sb.host_flags)
                     else:
-                        (sa,), _ = split_many_device([A[i0:i1, lo:hi]], cfg.type2, params, emu, check=eager)
+                        (sa,), _ = split_many_device([A[i0:i1, lo:hi]], cfg.type2, params, emu, check=eager,
+                                                     **fx)
                     hfa.append(sa.host_flags)
                     s_a, s_b = max(s_a, sa.s), max(s_b, sb.s)
                     s_dev = None
@@ -283,7 +311,7 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
                 if host_out is not None and last and mp == m and np_ == n:
                     host = (host_out, _copy_stream(torch).cuda_stream)
                 _pair_pass(torch, cfg, sa, sb, i1 - i0, j1 - j0, kb, order, cutoff, emu, bi, C, i0, j0, n,
-                           gflags[bi:bi + 1], sp, host, s_dev)
+                           gflags[bi:bi + 1], sp, host, s_dev, group_max(params, kb) if fixed else 0)
                 if timing:
                     ev[2].record()
                     evs.append(ev)
@@ -344,12 +372,13 @@ def _copy_stream(torch):
 
 
 def _pair_pass(torch, cfg, sa, sb, m, n, kb, order, cutoff, emu, bi, C, i0, j0, ldc, flags, sp, host=None,
-               s_dev=None):
-    """One fused pair-GEMM launch for the C panel [i0:i0+m, j0:j0+n]."""
+               s_dev=None, gmax=0):
+    """One fused pair-GEMM launch for the C panel [i0:i0+m, j0:j0+n]; gmax > 0:
+    fixed-step slices, up to gmax pairs of an anti-diagonal per accumulator."""
     sx = min(sa.s, cfg.max_slices or sa.s)
     sy = min(sb.s, cfg.max_slices or sb.s)
     tca = tcb = None
-    if cfg.skip_zero_pairs and m and n:
+    if cfg.skip_zero_pairs and m and n and not gmax:
         tca = torch.empty((m + 127) // 128, dtype=torch.int32, device=C.device)
         tcb = torch.empty((n + 127) // 128, dtype=torch.int32, device=C.device)
         _lib.call("oz_tile_counts", sa.row_cnt.data_ptr(), m, tca.data_ptr(), sp)
@@ -363,6 +392,17 @@ def _pair_pass(torch, cfg, sa, sb, m, n, kb, order, cutoff, emu, bi, C, i0, j0, 
         ws.record_stream(cs)
         C.record_stream(cs)
     Cp = C[i0:, j0:] if (i0 or j0) else C
+    if gmax:
+        _lib.call("oz_pair_gemm_grouped",
+                  sa.planes.data_ptr() if sa.s else None, sb.planes.data_ptr() if sb.s else None,
+                  sa.ld, sb.ld, sa.s, sb.s,
+                  sa.expo.data_ptr() if sa.s else None, sb.expo.data_ptr() if sb.s else None,
+                  m, n, kb, sx, sy, _lib.FMT_CODE[cfg.type2.name], order, cutoff, gmax, int(emu),
+                  int(bi > 0), Cp.data_ptr(), ldc, flags.data_ptr(),
+                  ws.data_ptr(), ws_bytes, PACE_SLACK,
+                  host[0].data_ptr() if host else None, host[0].shape[1] if host else 0,
+                  host[1] if host else None, s_dev.data_ptr() if s_dev is not None else None, sp)
+        return
     _lib.call("oz_pair_gemm",
               sa.planes.data_ptr() if sa.s else None, sb.planes.data_ptr() if sb.s else None,
               sa.ld, sb.ld, sa.s, sb.s,

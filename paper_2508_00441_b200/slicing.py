@@ -190,8 +190,19 @@ def _plane_cap(rows: int, row_bytes: int, predicted: int) -> int:
     return max(cap, min(predicted + 4, PLANE_CAP), 1)
 
 
+def _split_launch(fixed: bool, max_planes: int, X, rows, kb, ldx, code, rho, emu, cap, planes, ld, expo, row_cnt,
+                  s_ptr, f_ptr, sp):
+    """oz_split_fused (reference exponents) or oz_split_fixed (fixed-step extension)."""
+    if fixed:
+        _lib.call("oz_split_fixed", X.data_ptr(), rows, kb, ldx, code, rho, int(emu), cap, max_planes, planes, ld,
+                  expo, row_cnt.data_ptr(), s_ptr, f_ptr, sp)
+    else:
+        _lib.call("oz_split_fused", X.data_ptr(), rows, kb, ldx, code, rho, int(emu), cap, planes, ld, expo,
+                  row_cnt.data_ptr(), s_ptr, f_ptr, sp)
+
+
 def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, stream=None,
-                      check: bool = True, flags_out=None):
+                      check: bool = True, flags_out=None, fixed: bool = False, max_planes: int = 0):
     """Slice several matrices with one host synchronisation.
 
     Fast path: one fused pass per matrix (``oz_split_fused``) writes the slices
@@ -201,7 +212,9 @@ def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, str
     re-sliced exactly with the two-pass path (count, then write s planes).
     Flags are checked in argument order (the reference slices A before B).
     Representability flags go to the device word ``flags_out`` if given
-    (checked later by the caller), else they are checked here."""
+    (checked later by the caller), else they are checked here.  ``fixed``:
+    fixed-step exponents (oz_split_fixed, opt-in extension), at most
+    ``max_planes`` slices per row when > 0."""
     torch = _lib.require_cuda()
     if not params.feasible:
         raise SlicingInfeasible(
@@ -219,13 +232,14 @@ def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, str
         ldx = X.stride(0) if rows > 1 else kb
         ld = _row_len(kb, fmt)
         cap = _plane_cap(rows, _row_bytes(ld, fmt), predicted)
+        if fixed and max_planes > 0:
+            cap = min(cap, max_planes)
         row_cnt = torch.zeros(max(rows, 1), dtype=torch.int32, device=X.device)
         planes = torch.empty((cap, rows, _row_bytes(ld, fmt)), dtype=torch.uint8, device=X.device)
         expo = torch.empty((cap, rows), dtype=torch.int32, device=X.device)
         if rows > 0:
-            _lib.call("oz_split_fused", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu), cap,
-                      planes.data_ptr(), ld, expo.data_ptr(), row_cnt.data_ptr(),
-                      small.data_ptr() + 8 * i, small.data_ptr() + 8 * i + 4, sp)
+            _split_launch(fixed, max_planes, X, rows, kb, ldx, code, params.rho, emu, cap, planes.data_ptr(), ld,
+                          expo.data_ptr(), row_cnt, small.data_ptr() + 8 * i, small.data_ptr() + 8 * i + 4, sp)
         metas.append((X, rows, kb, ldx, ld, row_cnt, planes, expo))
     host = small.cpu().tolist()  # the one synchronisation
     out, all_flags = [], 0
@@ -235,8 +249,12 @@ def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, str
             # Some row needs more planes than allocated: exact two-pass split.
             del planes, expo
             cnt = torch.zeros(2, dtype=torch.int32, device=X.device)
-            _lib.call("oz_split_count", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu),
-                      row_cnt.data_ptr(), cnt.data_ptr(), cnt.data_ptr() + 4, sp)
+            if fixed:  # count-only mode of the fixed-step split (no planes)
+                _split_launch(True, max_planes, X, rows, kb, ldx, code, params.rho, emu, 0, None, ld, None,
+                              row_cnt, cnt.data_ptr(), cnt.data_ptr() + 4, sp)
+            else:
+                _lib.call("oz_split_count", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu),
+                          row_cnt.data_ptr(), cnt.data_ptr(), cnt.data_ptr() + 4, sp)
             s_max, flags = (int(v) for v in cnt.cpu().tolist())
             flags &= 0xFFFFFFFF
             if check:
@@ -245,9 +263,16 @@ def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, str
             expo = torch.empty((s_max, rows), dtype=torch.int32, device=X.device)
             if s_max > 0:
                 fw = torch.zeros(1, dtype=torch.int32, device=X.device)
-                _lib.call("oz_split_rows", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu), s_max,
-                          planes.data_ptr(), ld, expo.data_ptr(), row_cnt.data_ptr(),
-                          (flags_out if flags_out is not None else fw).data_ptr(), sp)
+                fwp = (flags_out if flags_out is not None else fw).data_ptr()
+                if fixed:
+                    s_scr = torch.zeros(1, dtype=torch.int32, device=X.device)
+                    _split_launch(True, max_planes, X, rows, kb, ldx, code, params.rho, emu, s_max,
+                                  planes.data_ptr(), ld, expo.data_ptr(), row_cnt, s_scr.data_ptr(), fwp, sp)
+                    _lib.call("oz_split_pad", planes.data_ptr(), ld, rows, code, s_max, None, row_cnt.data_ptr(),
+                              None, sp)
+                else:
+                    _lib.call("oz_split_rows", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu), s_max,
+                              planes.data_ptr(), ld, expo.data_ptr(), row_cnt.data_ptr(), fwp, sp)
                 if flags_out is None:
                     flags |= int(fw.item()) & 0xFFFFFFFF  # representability (write pass only)
                     if check:
@@ -266,14 +291,15 @@ def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, str
                     _lib.raise_for_flags(rep, "split")
             planes, expo = planes[:s_max], expo[:s_max]
             if s_max > 0 and rows > 0:
-                _lib.call("oz_split_pad", planes.data_ptr(), ld, rows, code, s_max, expo.data_ptr(),
-                          row_cnt.data_ptr(), None, sp)
+                _lib.call("oz_split_pad", planes.data_ptr(), ld, rows, code, s_max,
+                          None if fixed else expo.data_ptr(), row_cnt.data_ptr(), None, sp)
         all_flags |= flags
         out.append(DeviceSlices(planes, expo, row_cnt[:rows], s_max, rows, kb, ld, fmt, host_flags=full))
     return out, all_flags
 
 
-def split_deferred(X, fmt: FormatSpec, params: SlicingParams, emu: bool, stream=None) -> DeviceSlices:
+def split_deferred(X, fmt: FormatSpec, params: SlicingParams, emu: bool, stream=None, fixed: bool = False,
+                   max_planes: int = 0) -> DeviceSlices:
     """One-pass split without a host synchronisation: the fused split and the
     zero padding (which reads s on the device) are only enqueued.  The result
     holds ``cap`` planes; the pair GEMM takes the true s from ``sf`` on the
@@ -289,15 +315,17 @@ def split_deferred(X, fmt: FormatSpec, params: SlicingParams, emu: bool, stream=
     ldx = X.stride(0) if rows > 1 else kb
     ld = _row_len(kb, fmt)
     cap = _plane_cap(rows, _row_bytes(ld, fmt), predict_slice_count(params) or 1)
+    if fixed and max_planes > 0:
+        cap = min(cap, max_planes)
     sf = torch.zeros(2, dtype=torch.int32, device=X.device)
     row_cnt = torch.empty(max(rows, 1), dtype=torch.int32, device=X.device)
     planes = torch.empty((cap, rows, _row_bytes(ld, fmt)), dtype=torch.uint8, device=X.device)
     expo = torch.empty((cap, rows), dtype=torch.int32, device=X.device)
     if rows > 0:
-        _lib.call("oz_split_fused", X.data_ptr(), rows, kb, ldx, code, params.rho, int(emu), cap,
-                  planes.data_ptr(), ld, expo.data_ptr(), row_cnt.data_ptr(), sf.data_ptr(), sf.data_ptr() + 4, sp)
-        _lib.call("oz_split_pad", planes.data_ptr(), ld, rows, code, cap, expo.data_ptr(), row_cnt.data_ptr(),
-                  sf.data_ptr(), sp)
+        _split_launch(fixed, max_planes, X, rows, kb, ldx, code, params.rho, emu, cap, planes.data_ptr(), ld,
+                      expo.data_ptr(), row_cnt, sf.data_ptr(), sf.data_ptr() + 4, sp)
+        _lib.call("oz_split_pad", planes.data_ptr(), ld, rows, code, cap, None if fixed else expo.data_ptr(),
+                  row_cnt.data_ptr(), sf.data_ptr(), sp)
     return DeviceSlices(planes, expo, row_cnt[:rows], cap, rows, kb, ld, fmt, sf)
 
 

@@ -258,3 +258,68 @@ def test_lp_gemm_fp6_exact(cuda):
         for q in (0, sb.s - 1):
             G = oz.lp_gemm(oz.LpMatrix(sa.coeff[p], f), oz.LpMatrix(sb.coeff[q], f), oz.get_format("fp32"))
             assert np.array_equal(G, sa.coeff[p] @ sb.coeff[q])
+
+
+FIXED_CASES = [
+    # m, n, k, phi, type2, k_block, emu, max_slices, order, cutoff
+    (128, 128, 128, 0.5, "fp8e4m3", 0, False, None, "smallest-first", None),
+    (300, 260, 1000, 1.0, "fp8e4m3", 0, False, None, "smallest-first", 11),
+    (257, 200, 700, 4.0, "fp8e4m3", 0, True, None, "smallest-first", 10),
+    (200, 136, 640, 0.5, "fp8e4m3", 256, False, None, "largest-first", None),
+    (129, 257, 333, 2.0, "fp8e4m3", 0, False, 6, "smallest-first", None),
+    (256, 128, 512, 0.5, "fp16", 0, False, None, "smallest-first", 6),
+    (160, 96, 700, 4.0, "fp16", 300, True, None, "smallest-first", None),
+    (64, 64, 96, 1.0, "bf16", 0, False, None, "smallest-first", None),
+]
+
+
+@pytest.mark.parametrize("case", FIXED_CASES, ids=[f"{c[0]}x{c[1]}x{c[2]}-{c[4]}-kb{c[5]}-emu{int(c[6])}"
+                                                   f"-ms{c[7]}-{c[8][:5]}-cut{c[9]}" for c in FIXED_CASES])
+@pytest.mark.parametrize("variant", [("1", "128"), ("2", "128"), ("2", "192")], ids=lambda v: f"cta{v[0]}-n{v[1]}")
+def test_fixed_step_grouped_bitwise(cuda, case, variant, pair_variant):
+    """slice_exponents="fixed" (opt-in): fixed-step slices and level-grouped
+    tensor-core accumulation, bitwise against the CPU restatement
+    (oracle.oz_gemm_fixed), in every kernel variant and both FP64 modes."""
+    import oracle
+
+    pair_variant(int(variant[0]), int(variant[1]))
+    oz = _oz()
+    m, n, k, phi, t2, kbk, emu, ms, order, cut = case
+    rng = np.random.default_rng(m * 3 + n * 5 + k)
+    A = spread_matrix(rng, m, k, phi)
+    B = spread_matrix(rng, k, n, phi)
+    cfg = oz.GemmConfig(oz.get_format(t2), oz.get_format("fp32"), k_block=kbk, fp64_emulation=emu,
+                        max_slices=ms, accumulation_order=order, pair_cutoff=cut, slice_exponents="fixed")
+    res = oz.oz_gemm(A, B, cfg)
+    Cref, blocks = oracle.oz_gemm_fixed(A, B, t2, "fp32", kbk, ms, order, cut)
+    assert [(b.k_lo, b.k_hi, b.s_x, b.s_y) for b in res.stats.blocks] == blocks
+    nbad = int(np.sum(bits(res.C) != bits(Cref)))
+    assert nbad == 0, f"{nbad}/{m * n} entries differ"
+
+
+@pytest.mark.parametrize("fmt", ["fp8e4m3", "fp16"])
+@pytest.mark.parametrize("emu", [False, True])
+def test_fixed_step_split_bitwise(cuda, fmt, emu):
+    """oz_split_fixed: slices and exponents (incl. the continued exponent
+    sequence of padding planes) equal the CPU restatement; the slices
+    reconstruct the input exactly."""
+    import oracle
+    from paper_2508_00441_b200.slicing import split_many_device
+
+    torch = cuda
+    oz = _oz()
+    rng = np.random.default_rng(31)
+    X = spread_matrix(rng, 90, 700, 3.0)
+    X[5] = 0.0
+    X[7, :] = 1.0  # a row that ends after one slice
+    f = oz.get_format(fmt)
+    params = oz.compute_params(53, f.mant_bits, 24, 700)
+    (ds,), _ = split_many_device([torch.from_numpy(X).cuda()], f, params, emu, fixed=True)
+    ss = oz.slicing.device_to_sliceset(ds, "rows", params)
+    coeff, expo, cnt, s = oracle.split_rows_fixed(X, params.rho)
+    assert ss.s == s
+    for p in range(s):
+        assert np.array_equal(bits(ss.coeff[p]), bits(coeff[p])), p
+        assert np.array_equal(ss.expo[p], expo[p]), p
+    rec = sum(np.ldexp(coeff[p], expo[p][:, None]) for p in range(s))
+    assert np.array_equal(bits(rec), bits(X))

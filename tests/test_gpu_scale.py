@@ -101,6 +101,31 @@ def test_sampled_blocks_bitwise_multiwave(cuda, case):
     assert nbad == 0, f"{nbad} of {Cs.size} sampled entries differ"
 
 
+@pytest.mark.parametrize("cut,emu", [(11, False), (10, True), (None, False)])
+def test_fixed_step_sampled_blocks_n8192(cuda, cut, emu):
+    """The opt-in fast mode (fixed-step slices, level-grouped accumulation) at the
+    headline size: sampled C blocks over all tile waves, bitwise against the CPU
+    restatement on the same A rows / B columns."""
+    torch = cuda
+    import oracle
+    import paper_2508_00441_b200 as oz
+
+    n = 8192
+    A, B = device_inputs(torch, n, 0.5, 4242)
+    cfg = oz.GemmConfig(oz.get_format("fp8e4m3"), oz.get_format("fp32"), fp64_emulation=emu, pair_cutoff=cut,
+                        slice_exponents="fixed")
+    C, st = oz.oz_gemm_device(A, B, cfg)
+    rows, cols = sample_index(n), sample_index(n)
+    Cs = C[rows][:, cols].cpu().numpy()
+    # pad the sample's slices to the full problem's counts: pair groups then match
+    Cref, blocks = oracle.oz_gemm_fixed(A[rows].cpu().numpy(), B[:, cols].cpu().numpy(), "fp8e4m3", "fp32", 0,
+                                        None, "smallest-first", cut,
+                                        pad_to=[(st.blocks[0].s_x, st.blocks[0].s_y)])
+    assert (blocks[0][2], blocks[0][3]) == (st.blocks[0].s_x, st.blocks[0].s_y)
+    nbad = int(np.sum(Cs.view(np.uint64) != Cref.view(np.uint64)))
+    assert nbad == 0, f"{nbad} of {Cs.size} sampled entries differ"
+
+
 def test_full_c_deterministic(cuda):
     torch = cuda
     import paper_2508_00441_b200 as oz
