@@ -543,7 +543,8 @@ def run_variants(args, torch, oz, A, B, Cdd, d, nz, c_cublas, dev, steps=3):
 
     def one(name, cfg, A_, B_, dd=None, mask=None, cub=None):
         ms, st = _time_steps(torch, oz, A_, B_, cfg, steps)
-        row = {"tflops": flops / (ms / 1e3) / 1e12, "ms": ms, "gemm_count": st.gemm_count,
+        row = {"tflops": flops / (ms / 1e3) / 1e12, "ms": ms, "kernel_ms": st.t_gemm * 1e3,
+               "split_ms": st.t_slice * 1e3, "gemm_count": st.gemm_count,
                "gemm_ops": st.gemm_ops, "blocks": len(st.blocks),
                "s": [(b.s_x, b.s_y) for b in st.blocks[:1]]}
         if dd is not None:
