@@ -80,6 +80,19 @@ int oz_split_fixed(const double* X, int64_t rows, int64_t kb, int64_t ldx, int t
                    int max_planes, void* coeff, int64_t ld_coeff, int32_t* expo, int32_t* row_cnt, int32_t* s_max,
                    uint32_t* flags, void* stream);
 
+/* oz_split_fixed for the COLUMNS of a row-major X[kb][cols] (leading dimension
+ * ldx), read in place: identical planes, exponents, counts, s and flags to
+ * transposing X (oz_transpose) and calling oz_split_fixed on X^T — the column
+ * slicing of slice_matrix(..., "cols") (slicing.py:199-203) without the
+ * transposed FP64 copy.  Requires max_planes >= 1 (the plane-limited fast mode).
+ * scratch: oz_split_fixed_cols_scratch(cols) bytes of device memory (zeroed
+ * here on `stream`).  Pad with oz_split_pad(..., expo = NULL, ...) as for
+ * oz_split_fixed. */
+int64_t oz_split_fixed_cols_scratch(int64_t cols);
+int oz_split_fixed_cols(const double* X, int64_t kb, int64_t cols, int64_t ldx, int type2, int rho, int emu, int cap,
+                        int max_planes, void* coeff, int64_t ld_coeff, int32_t* expo, int32_t* col_cnt,
+                        int32_t* s_max, uint32_t* flags, void* scratch, void* stream);
+
 /* Zero slices for rows exhausted before the global s (slicing.py:149-152): for
  * every row r, planes [row_cnt[r], s) of coeff[.][rows][ld_coeff] are zeroed and
  * their exponents set to 0.  Completes oz_split_fused.  s_dev (nullable): read s

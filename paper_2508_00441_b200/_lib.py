@@ -39,6 +39,8 @@ _I = ctypes.c_int
 SIGNATURES = {
     "oz_split_fused": (_I, [_P, _I64, _I64, _I64, _I, _I, _I, _I, _P, _I64, _P, _P, _P, _P, _P]),
     "oz_split_fixed": (_I, [_P, _I64, _I64, _I64, _I, _I, _I, _I, _I, _P, _I64, _P, _P, _P, _P, _P]),
+    "oz_split_fixed_cols": (_I, [_P, _I64, _I64, _I64, _I, _I, _I, _I, _I, _P, _I64, _P, _P, _P, _P, _P, _P]),
+    "oz_split_fixed_cols_scratch": (ctypes.c_int64, [_I64]),
     "oz_split_pad": (_I, [_P, _I64, _I64, _I, _I, _P, _P, _P, _P]),
     "oz_split_count": (_I, [_P, _I64, _I64, _I64, _I, _I, _I, _P, _P, _P, _P]),
     "oz_split_rows": (_I, [_P, _I64, _I64, _I64, _I, _I, _I, _I, _P, _I64, _P, _P, _P, _P]),

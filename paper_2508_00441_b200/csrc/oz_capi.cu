@@ -316,6 +316,45 @@ int oz_split_fixed(const double* X, int64_t rows, int64_t kb, int64_t ldx, int t
                     s_max, flags, stream);
 }
 
+int64_t oz_split_fixed_cols_scratch(int64_t cols) { return cols > 0 ? 3 * 4 * cols : 0; }
+
+int oz_split_fixed_cols(const double* X, int64_t kb, int64_t cols, int64_t ldx, int type2, int rho, int emu, int cap,
+                        int max_planes, void* coeff, int64_t ld_coeff, int32_t* expo, int32_t* col_cnt,
+                        int32_t* s_max, uint32_t* flags, void* scratch, void* stream) {
+  LpFormat f;
+  uint32_t idf;
+  if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
+  if (rho < 42 || rho > 53) return OZ_EUNSUPPORTED;
+  if (kb < 1 || cols < 0 || ldx < cols || ld_coeff < kb || cap < 0 || max_planes < 1 || !X || !col_cnt ||
+      !s_max || !flags)
+    return OZ_EINVAL;
+  if ((ld_coeff * f.bytes) % 16) return OZ_EINVAL;
+  if (cols == 0) return OZ_OK;
+  if (!scratch || (cap > 0 && (!coeff || !expo))) return OZ_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  oz::ColSplitParams P{};
+  P.X = X; P.kb = kb; P.cols = cols; P.ldx = ldx; P.rho = rho; P.w = 54 - rho; P.max_planes = max_planes;
+  P.cap = cap; P.coeff = cap > 0 ? static_cast<uint8_t*>(coeff) : nullptr; P.ld = ld_coeff; P.expo = expo;
+  P.col_cnt = col_cnt; P.s_max = s_max; P.flags = flags; P.kmax = 1 << (53 - rho);
+  P.pack6 = (type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3) ? 1 : 0;
+  if (P.pack6 && (ld_coeff & 127)) return OZ_EINVAL;
+  int rc = code_table(type2, f, rho, st, &P.table, &P.table_clean);
+  if (rc) return rc;
+  P.key = static_cast<uint32_t*>(scratch);
+  P.need = P.key + cols;
+  P.tiny = P.need + cols;
+  if (cudaMemsetAsync(scratch, 0, (size_t)oz_split_fixed_cols_scratch(cols), st) != cudaSuccess) return OZ_ECUDA;
+  const dim3 grid((unsigned)((cols + oz::kColTJ - 1) / oz::kColTJ), (unsigned)((kb + oz::kColTK - 1) / oz::kColTK));
+  oz::col_stats_kernel<<<grid, 256, 0, st>>>(P);
+  const size_t smem = sizeof(uint32_t) * (2 * P.kmax + 1);
+  auto kern = f.bytes == 1 ? (emu ? oz::col_slice_kernel<1, true> : oz::col_slice_kernel<1, false>)
+                           : (emu ? oz::col_slice_kernel<2, true> : oz::col_slice_kernel<2, false>);
+  if (smem > 8 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<grid, 256, smem, st>>>(P);
+  oz::col_finish_kernel<<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(P);
+  return launch_status();
+}
+
 }  // extern "C"
 
 namespace {

@@ -189,7 +189,9 @@ OZ_DEVICE uint64_t emu_slice_elem(uint64_t x, int g, int& k) {
 // returns the next max key.  kWrite: emit the 16-byte plane vectors; kChecked:
 // per-element subnormal-residual and representability checks (only needed for
 // rows holding inputs below 2^-969, or code tables with unrepresentable entries).
-template <int kThreads, int kEPT, int kEB, bool kEmu, bool kWrite, bool kChecked>
+// kKey = false (fixed-step fast path, kWrite only): return the OR of the codes
+// instead of the max key (the row max is not needed there).
+template <int kThreads, int kEPT, int kEB, bool kEmu, bool kWrite, bool kChecked, bool kKey = true>
 OZ_DEVICE uint32_t slice_iteration(uint64_t (&x)[kEPT], const uint64_t sigma, const int g, const uint32_t* __restrict__ tblc,
                                    int K, uint8_t* plane, int64_t base, int t, int64_t ld, uint32_t& flags,
                                    uint32_t& bad, const int pack6) {
@@ -223,10 +225,11 @@ OZ_DEVICE uint32_t slice_iteration(uint64_t (&x)[kEPT], const uint64_t sigma, co
         if constexpr (kChecked) bad |= ent;
         codes[u] = ent;
       }
-      key = max(key, elem_key(xn));
+      if constexpr (kKey) key = max(key, elem_key(xn));
+      else key |= codes[u];
       if constexpr (kChecked) {
         const uint32_t ef = (uint32_t)((xn >> 52) & 0x7FF);
-        if (ef == 0 && (xn << 1) != 0) flags |= FLAG_SUBNORMAL_RESID;
+        if (ef == 0 && ((uint32_t)xn | ((uint32_t)(xn >> 32) << 1)) != 0u) flags |= FLAG_SUBNORMAL_RESID;
       }
     }
     if constexpr (kWrite) {
@@ -329,23 +332,85 @@ __global__ void __launch_bounds__(kThreads, kThreads <= 256 ? 2 : 1) split_fused
   uint8_t* const row_plane0 = P.coeff + row * row_bytes;
   const uint32_t* tblc = tbl + K;
   const bool write = P.coeff != nullptr;  // count-only mode otherwise (no planes, no exponents)
-  int cnt = 0;
-  int c_prev = 0;
-  for (int it = 0;; ++it) {
-    // Row max of the key: warp redux -> smem -> (cluster DSMEM).
-    uint32_t m = __reduce_max_sync(0xFFFFFFFFu, key);
-    if (lane == 0) red_w[it & 1][wid] = m;
+  // Row max of a u32: warp redux -> smem -> (cluster DSMEM); slot alternates
+  // between consecutive calls so one barrier per call suffices.
+  auto row_max = [&](uint32_t v, int slot) -> uint32_t {
+    uint32_t m = __reduce_max_sync(0xFFFFFFFFu, v);
+    if (lane == 0) red_w[slot & 1][wid] = m;
     __syncthreads();
     m = 0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) m = max(m, red_w[it & 1][w]);
+    for (int w = 0; w < kWarps; ++w) m = max(m, red_w[slot & 1][w]);
     if constexpr (kCL > 1) {
-      if (t < kCL) st_cluster_u32(&red_c[it & 1][rank], (uint32_t)t, m);
+      if (t < kCL) st_cluster_u32(&red_c[slot & 1][rank], (uint32_t)t, m);
       cluster_barrier();
       m = 0;
 #pragma unroll
-      for (int r = 0; r < kCL; ++r) m = max(m, red_c[it & 1][r]);
+      for (int r = 0; r < kCL; ++r) m = max(m, red_c[slot & 1][r]);
     }
+    return m;
+  };
+  int cnt = 0;
+  int c_prev = 0;
+  if (P.fixed_w > 0 && P.max_planes > 0) {
+    // Fixed-step exponents with a plane limit: every exponent follows from the
+    // first row max, so the iterations need no row reductions at all.  Each
+    // thread slices its elements through L planes; the row count (the
+    // reference loop's exit at the first all-zero residual, slicing.py:149-152)
+    // is recovered afterwards from the per-thread count of leading non-zero
+    // iterations (a zero residual stays zero and slices to code 0, so planes a
+    // short row writes past its count are the zero padding it would get anyway).
+    const uint32_t m0 = row_max(key, 0);
+    if (m0 != 0) {
+      const int e = (int)(m0 >> 21) - 1023;
+      const int c0 = (m0 & 0x1FFFFFu) != 0 ? e + 1 : e;
+      c_prev = c0;
+      // L = planes the reference loop may produce before a limit check fires at
+      // iteration L (same order as below: plane limit, allocation, sigma range).
+      int L = 0;
+      const int lim = write ? min(P.max_planes, P.cap) : P.max_planes;
+      while (L < lim) {
+        const int se = c0 - L * P.fixed_w + P.rho - 1 + 1023;
+        if (se < 1 || se > 2046) break;
+        ++L;
+      }
+      // Iterations this thread's elements need: with codes written, a residual
+      // entering iteration it is non-zero exactly when a code of an iteration
+      // >= it or the final residual is non-zero (count-only mode: the key).
+      int z = 0;
+      for (int it = 0; it < L; ++it) {
+        const int c = c0 - it * P.fixed_w;
+        const uint64_t sigma = ((uint64_t)(c + P.rho - 1 + 1023) << 52) | (1ull << 51);
+        uint8_t* plane = row_plane0 + (int64_t)it * plane_stride;
+        if (!write) {
+          if (key != 0) z = it + 1;
+          key = slice_iteration<kThreads, kEPT, kEB, kEmu, false, true>(x, sigma, c + P.rho - 53, tblc, K, plane, base,
+                                                                        t, P.ld, flags, bad, P.pack6);
+          continue;
+        }
+        const uint32_t cor =
+            checked ? slice_iteration<kThreads, kEPT, kEB, kEmu, true, true, false>(x, sigma, c + P.rho - 53, tblc, K,
+                                                                                   plane, base, t, P.ld, flags, bad,
+                                                                                   P.pack6)
+                    : slice_iteration<kThreads, kEPT, kEB, kEmu, true, false, false>(x, sigma, c + P.rho - 53, tblc, K,
+                                                                                    plane, base, t, P.ld, flags, bad,
+                                                                                    P.pack6);
+        bad |= cor;
+        if (cor & 0xFFFFu) z = it + 1;
+      }
+      uint32_t rest = 0;
+#pragma unroll
+      for (int i = 0; i < kEPT; ++i) rest |= (uint32_t)x[i] | ((uint32_t)(x[i] >> 32) << 1);
+      if (rest) z = L + 1;  // still non-zero where a limit check stops the loop
+      const int need = (int)row_max((uint32_t)z, 1);
+      cnt = min(need, L);
+      if (need > L && L < P.max_planes) flags |= (write && L >= P.cap) ? FLAG_PLANE_CAP_INTERNAL : FLAG_SIGMA_RANGE;
+      if (write && t == 0 && rank == 0)
+        for (int p = 0; p < cnt; ++p) P.expo[(int64_t)p * P.rows + row] = c0 - p * P.fixed_w;
+    }
+  } else
+  for (int it = 0;; ++it) {
+    const uint32_t m = row_max(key, it);
     if (m == 0) break;
     if (it >= kHardSlices) {
       flags |= FLAG_SLICE_CAP;
@@ -390,6 +455,252 @@ __global__ void __launch_bounds__(kThreads, kThreads <= 256 ? 2 : 1) split_fused
   }
   flags = __reduce_or_sync(0xFFFFFFFFu, flags);
   if (lane == 0 && flags) atomicOr(P.flags, flags);
+}
+
+// ─────────── K1c: fixed-step split of COLUMNS, read in place (no transpose) ───────────
+// Opt-in extension (GemmConfig.slice_exponents = "fixed" with a plane limit):
+// slices column j of a row-major X[kb][cols] exactly as split_fused_kernel's
+// fixed-step fast path slices row j of X^T, writing the same K-major planes
+// coeff[p][j][ld] — so B needs no transposed FP64 copy (1 GB of traffic at
+// n = 8192).  Three launches: per-column max key (atomics over k tiles), the
+// slicing of 256 x 16 tiles staged through XOR-swizzled shared memory (each
+// thread owns 16 consecutive k of one column, i.e. one 16-byte plane vector),
+// and a per-column finish (counts, exponents, s).
+struct ColSplitParams {
+  const double* X;
+  int64_t kb, cols, ldx;
+  int rho, w, max_planes, cap;
+  uint8_t* coeff;          // [cap][cols][ld] (nullptr: count only)
+  int64_t ld;              // elements per plane row
+  int32_t* expo;           // [cap][cols]
+  int32_t* col_cnt;        // [cols]
+  int32_t* s_max;
+  uint32_t* flags;
+  const uint32_t* table;   // as FusedSplitParams
+  int kmax, pack6, table_clean;
+  uint32_t* key;           // [cols] max element key (zeroed by the host)
+  uint32_t* need;          // [cols] iterations the column needs (max over tiles; zeroed)
+  uint32_t* tiny;          // [cols] 1: holds an input below 2^-969 (checked slicing)
+};
+
+constexpr int kColTK = 256, kColTJ = 16;  // tile: 256 k x 16 columns
+
+OZ_DEVICE int col_c0(uint32_t m) {
+  const int e = (int)(m >> 21) - 1023;
+  return (m & 0x1FFFFFu) != 0 ? e + 1 : e;
+}
+
+// Planes column j may produce (same limit order as the row kernel).
+OZ_DEVICE int col_limit(const ColSplitParams& P, int c0) {
+  const int lim = P.coeff ? min(P.max_planes, P.cap) : P.max_planes;
+  int L = 0;
+  while (L < lim) {
+    const int se = c0 - L * P.w + P.rho - 1 + 1023;
+    if (se < 1 || se > 2046) break;
+    ++L;
+  }
+  return L;
+}
+
+__global__ void __launch_bounds__(256) col_stats_kernel(const ColSplitParams P) {
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t j = (int64_t)blockIdx.x * kColTJ + tx;
+  const int64_t k0 = (int64_t)blockIdx.y * kColTK;
+  uint32_t key = 0, flags = 0;
+  bool tiny = false;
+  if (j < P.cols) {
+#pragma unroll 4
+    for (int i = ty; i < kColTK; i += 16) {
+      const int64_t k = k0 + i;
+      if (k >= P.kb) break;
+      const uint64_t x = reinterpret_cast<const uint64_t*>(P.X)[k * P.ldx + j];
+      const uint32_t ef = (uint32_t)((x >> 52) & 0x7FF);
+      if (ef == 2047) {
+        flags |= FLAG_NONFINITE_INPUT;  // sliced as zero; the host raises (slicing.py:119-122)
+        continue;
+      }
+      if (ef == 0 && (x << 1) != 0) flags |= FLAG_SUBNORMAL_INPUT;
+      if (ef < 1023 - 969 && (x << 1) != 0) tiny = true;
+      key = max(key, elem_key(x));
+    }
+  }
+  __shared__ uint32_t sk[16][17], st[16][17];
+  sk[ty][tx] = key;
+  st[ty][tx] = tiny ? 1u : 0u;
+  __syncthreads();
+  if (ty == 0 && j < P.cols) {
+    uint32_t m = 0, ti = 0;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      m = max(m, sk[r][tx]);
+      ti |= st[r][tx];
+    }
+    if (m) atomicMax(P.key + j, m);
+    if (ti) atomicOr(P.tiny + j, 1u);
+  }
+  flags = __reduce_or_sync(0xFFFFFFFFu, flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(P.flags, flags);
+}
+
+// The plane loop of one thread (16 consecutive k of one column): returns the
+// iterations its elements need (L + 1 if a residual is still non-zero after L).
+// A residual entering iteration `it` is non-zero exactly when some code of an
+// iteration >= it or the final residual is non-zero, so the count comes from
+// the codes (no per-element zero test).
+template <int kEB, bool kEmu, bool kChecked, bool kPack6>
+OZ_DEVICE int col_slice_planes(const ColSplitParams& P, uint64_t (&x)[16], int c0, int L, const uint32_t* tblc,
+                               int K, uint8_t* dst0, int64_t plane_stride, int nvec, uint32_t& flags) {
+  constexpr int kV = 16 / kEB;
+  uint32_t bad = 0;
+  int z = 0;
+  for (int it = 0; it < L; ++it) {
+    const int c = c0 - it * P.w;
+    const int g = c + P.rho - 53;
+    const uint64_t sigma = ((uint64_t)(c + P.rho - 1 + 1023) << 52) | (1ull << 51);
+    uint32_t codes[16];
+    uint32_t cor = 0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      uint64_t xn;
+      int k;
+      if constexpr (kEmu && !kChecked) {
+        xn = emu_slice_elem(x[u], g, k);
+      } else if constexpr (kEmu) {
+        const uint64_t xs = emu_add(x[u], sigma, flags);
+        const uint64_t v = emu_add(xs, sigma ^ kSign, flags);
+        xn = emu_add(x[u], v ^ kSign, flags);
+        k = min(max((int)(uint32_t)xs, -K), K);
+      } else {
+        const double xsd = __dadd_rn(u2d(x[u]), u2d(sigma));
+        k = (int)(uint32_t)d2u(xsd);
+        xn = d2u(__dsub_rn(u2d(x[u]), __dsub_rn(xsd, u2d(sigma))));
+      }
+      x[u] = xn;
+      codes[u] = tblc[k];
+      cor |= codes[u];
+      if constexpr (kChecked) {
+        if (((uint32_t)(xn >> 52) & 0x7FFu) == 0u && ((uint32_t)xn | ((uint32_t)(xn >> 32) << 1)) != 0u)
+          flags |= FLAG_SUBNORMAL_RESID;
+      }
+    }
+    bad |= cor;
+    if (cor & 0xFFFFu) z = it + 1;
+    if (dst0) {
+      uint8_t* dst = dst0 + (int64_t)it * plane_stride;
+      if constexpr (kPack6) {
+        uint32_t q[3] = {0u, 0u, 0u};
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const uint32_t c6 = codes[u] & 63u, bit = 6u * (uint32_t)u;
+          q[bit >> 5] |= c6 << (bit & 31u);
+          if ((bit & 31u) > 26u) q[(bit >> 5) + 1] |= c6 >> (32u - (bit & 31u));
+        }
+        uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+        d[0] = q[0];
+        d[1] = q[1];
+        d[2] = q[2];
+      } else {
+#pragma unroll
+        for (int h = 0; h < 16 / kV; ++h) {
+          uint4 v;
+          const uint32_t* cc = codes + h * kV;
+          if constexpr (kEB == 1) {
+            v.x = __byte_perm(__byte_perm(cc[0], cc[1], 0x0040), __byte_perm(cc[2], cc[3], 0x0040), 0x5410);
+            v.y = __byte_perm(__byte_perm(cc[4], cc[5], 0x0040), __byte_perm(cc[6], cc[7], 0x0040), 0x5410);
+            v.z = __byte_perm(__byte_perm(cc[8], cc[9], 0x0040), __byte_perm(cc[10], cc[11], 0x0040), 0x5410);
+            v.w = __byte_perm(__byte_perm(cc[12], cc[13], 0x0040), __byte_perm(cc[14], cc[15], 0x0040), 0x5410);
+          } else {
+            v.x = __byte_perm(cc[0], cc[1], 0x5410);
+            v.y = __byte_perm(cc[2], cc[3], 0x5410);
+            v.z = __byte_perm(cc[4], cc[5], 0x5410);
+            v.w = __byte_perm(cc[6], cc[7], 0x5410);
+          }
+          if (h < nvec) reinterpret_cast<uint4*>(dst)[h] = v;
+        }
+      }
+    }
+  }
+  uint32_t rest = 0;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) rest |= (uint32_t)x[u] | ((uint32_t)(x[u] >> 32) << 1);
+  if (rest) z = L + 1;  // still non-zero where a limit check stops the loop
+  if (bad & (1u << 16)) flags |= FLAG_NOT_REPRESENTABLE;
+  return z;
+}
+
+template <int kEB, bool kEmu>
+__global__ void __launch_bounds__(256) col_slice_kernel(const ColSplitParams P) {
+  __shared__ uint64_t tile[kColTK * kColTJ];  // element (k, j) at k*16 + (j ^ (k >> 4 & 15))
+  extern __shared__ uint32_t tbl[];
+  const int t = threadIdx.x;
+  const int64_t j0 = (int64_t)blockIdx.x * kColTJ, k0 = (int64_t)blockIdx.y * kColTK;
+  const int K = P.kmax;
+  for (int i = t; i <= 2 * K; i += 256) tbl[i] = __ldg(P.table + i);
+  // Coalesced tile load: a warp reads two 128-byte row segments per step.
+  {
+    const int tx = t & 15, ty = t >> 4;
+    const int64_t j = j0 + tx;
+#pragma unroll 4
+    for (int i = ty; i < kColTK; i += 16) {
+      const int64_t k = k0 + i;
+      uint64_t x = (k < P.kb && j < P.cols) ? reinterpret_cast<const uint64_t*>(P.X)[k * P.ldx + j] : 0ull;
+      if (((x >> 52) & 0x7FF) == 0x7FF) x = 0;  // non-finite: flagged by col_stats
+      tile[i * 16 + (tx ^ ((i >> 4) & 15))] = x;
+    }
+  }
+  __syncthreads();
+  const int lane = t & 31, wid = t >> 5;
+  const int jl = 2 * wid + (lane >> 4), kseg = lane & 15;
+  const int64_t j = j0 + jl;
+  if (j >= P.cols) return;
+  const uint32_t m0 = __ldg(P.key + j);
+  if (m0 == 0) return;  // zero column: count 0, its planes are zero-padded later
+  uint64_t x[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) x[u] = tile[(16 * kseg + u) * 16 + (jl ^ kseg)];
+  const int c0 = col_c0(m0);
+  const int L = col_limit(P, c0);
+  const bool checked = __ldg(P.tiny + j) != 0 || !P.table_clean;
+  const uint32_t* tblc = tbl + K;
+  const int64_t e0 = k0 + 16 * kseg;
+  const int64_t row_bytes = P.pack6 ? P.ld * 3 / 4 : P.ld * kEB;
+  uint8_t* dst0 = (P.coeff && e0 < P.ld) ? P.coeff + j * row_bytes + (P.pack6 ? e0 / 16 * 12 : e0 * kEB) : nullptr;
+  const int64_t nv = (P.ld - e0) * kEB / 16;
+  const int nvec = nv < kEB ? (int)nv : kEB;  // 16-byte vectors of this thread inside the plane row
+  const int64_t plane_stride = P.cols * row_bytes;
+  uint32_t flags = 0;
+  int z;
+  if (kEB == 1 && P.pack6)
+    z = checked ? col_slice_planes<kEB, kEmu, true, true>(P, x, c0, L, tblc, K, dst0, plane_stride, nvec, flags)
+                : col_slice_planes<kEB, kEmu, false, true>(P, x, c0, L, tblc, K, dst0, plane_stride, nvec, flags);
+  else
+    z = checked ? col_slice_planes<kEB, kEmu, true, false>(P, x, c0, L, tblc, K, dst0, plane_stride, nvec, flags)
+                : col_slice_planes<kEB, kEmu, false, false>(P, x, c0, L, tblc, K, dst0, plane_stride, nvec, flags);
+  if (z) atomicMax(P.need + j, (uint32_t)z);
+  if (flags) atomicOr(P.flags, flags);
+}
+
+// Per column: count = min(needed iterations, L), limit flags, the exponent
+// sequence c0 - p w for every allocated plane, s = max count.
+__global__ void col_finish_kernel(const ColSplitParams P) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int cnt = 0;
+  if (j < P.cols) {
+    const uint32_t m0 = P.key[j];
+    const int c0 = m0 ? col_c0(m0) : 0;
+    if (m0) {
+      const int L = col_limit(P, c0);
+      const int need = (int)P.need[j];
+      cnt = min(need, L);
+      if (need > L && L < P.max_planes)
+        atomicOr(P.flags, (P.coeff && L >= P.cap) ? FLAG_PLANE_CAP_INTERNAL : FLAG_SIGMA_RANGE);
+    }
+    P.col_cnt[j] = cnt;
+    if (P.coeff)
+      for (int p = 0; p < P.cap; ++p) P.expo[(int64_t)p * P.cols + j] = c0 - p * P.w;
+  }
+  const int m = __reduce_max_sync(0xFFFFFFFFu, cnt);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(P.s_max, m);
 }
 
 // Zero slices for rows exhausted before the global s (slicing.py:149-152):

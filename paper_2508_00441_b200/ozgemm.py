@@ -287,14 +287,14 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
                     sa = split_deferred(A[i0:i1, lo:hi], cfg.type2, params, emu, **fx)
                     sfa.append(sa.sf)
                     if i0 == 0:
-                        Bt = transpose_device(B[lo:hi, j0:j1])
+                        Bt = _b_cols(B[lo:hi, j0:j1], fixed and max_planes > 0)
                         sb = split_deferred(Bt, cfg.type2, params, emu, **fx)
                         sfb.append(sb.sf)
                     s_dev = torch.cat([sa.sf[:1], sb.sf[:1]])
                 else:
                     eager = cfg.type2.name in _FP6  # FP6: raise split errors (SlicingInfeasible) right away
                     if i0 == 0:
-                        Bt = transpose_device(B[lo:hi, j0:j1])
+                        Bt = _b_cols(B[lo:hi, j0:j1], fixed and max_planes > 0)
                         (sa, sb), _ = split_many_device([A[i0:i1, lo:hi], Bt], cfg.type2, params, emu,
                                                         check=eager, **fx)
                         hfb.append(sb.host_flags)
@@ -361,6 +361,13 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
 
 _COPY_STREAMS = {}
 _FP6 = ("fp6e3m2", "fp6e2m3")
+
+
+def _b_cols(Bv, in_place: bool):
+    """B's column panel with columns as K-major rows: a transpose VIEW when the
+    fixed-step split reads columns in place (oz_split_fixed_cols), else the
+    device transpose (slicing.py:199-203 slices columns via the transpose)."""
+    return Bv.t() if in_place and (Bv.stride(1) == 1 or Bv.shape[1] == 1) else transpose_device(Bv)
 
 
 def _copy_stream(torch):

@@ -190,9 +190,33 @@ def _plane_cap(rows: int, row_bytes: int, predicted: int) -> int:
     return max(cap, min(predicted + 4, PLANE_CAP), 1)
 
 
+def _is_col_view(X) -> bool:
+    """X is the transpose view of a row-major matrix (its rows are columns):
+    sliced in place by oz_split_fixed_cols (fixed-step mode with a plane limit)."""
+    return X.shape[1] > 1 and X.stride(1) != 1 and (X.stride(0) == 1 or X.shape[0] == 1)
+
+
+def _check_view(X, fixed: bool, max_planes: int):
+    torch = _lib.require_cuda()
+    if X.dtype != torch.float64:
+        raise ValueError("split expects a float64 view")
+    if X.stride(1) != 1 and X.shape[1] > 1 and not (fixed and max_planes > 0 and _is_col_view(X)):
+        raise ValueError("split expects a float64 view with unit column stride (or, fixed-step mode with a "
+                         "plane limit, the transpose view of a row-major matrix)")
+
+
 def _split_launch(fixed: bool, max_planes: int, X, rows, kb, ldx, code, rho, emu, cap, planes, ld, expo, row_cnt,
                   s_ptr, f_ptr, sp):
-    """oz_split_fused (reference exponents) or oz_split_fixed (fixed-step extension)."""
+    """oz_split_fused (reference exponents) or oz_split_fixed (fixed-step extension);
+    a transpose view X = M[lo:hi, j0:j1].t() in fixed mode with a plane limit is
+    sliced column by column in place (oz_split_fixed_cols, no transposed copy).
+    The scratch tensor is allocated on, and used by, torch's current stream."""
+    if fixed and max_planes > 0 and _is_col_view(X):
+        torch = _lib.require_cuda()
+        scratch = torch.empty(max(3 * rows, 1), dtype=torch.int32, device=X.device)
+        _lib.call("oz_split_fixed_cols", X.data_ptr(), kb, rows, X.stride(1), code, rho, int(emu), cap, max_planes,
+                  planes, ld, expo, row_cnt.data_ptr(), s_ptr, f_ptr, scratch.data_ptr(), sp)
+        return
     if fixed:
         _lib.call("oz_split_fixed", X.data_ptr(), rows, kb, ldx, code, rho, int(emu), cap, max_planes, planes, ld,
                   expo, row_cnt.data_ptr(), s_ptr, f_ptr, sp)
@@ -227,8 +251,7 @@ def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, str
     small = torch.zeros(2 * len(Xs), dtype=torch.int32, device=Xs[0].device)  # [s, flags] per matrix
     for i, X in enumerate(Xs):
         rows, kb = X.shape
-        if X.dtype != torch.float64 or (X.stride(1) != 1 and kb > 1):
-            raise ValueError("split expects a float64 view with unit column stride")
+        _check_view(X, fixed, max_planes)
         ldx = X.stride(0) if rows > 1 else kb
         ld = _row_len(kb, fmt)
         cap = _plane_cap(rows, _row_bytes(ld, fmt), predicted)
@@ -310,8 +333,7 @@ def split_deferred(X, fmt: FormatSpec, params: SlicingParams, emu: bool, stream=
     sp = stream if stream is not None else _lib.stream_ptr(torch)
     eb = _lib.ELEM_BYTES[fmt.name]
     rows, kb = X.shape
-    if X.dtype != torch.float64 or (X.stride(1) != 1 and kb > 1):
-        raise ValueError("split expects a float64 view with unit column stride")
+    _check_view(X, fixed, max_planes)
     ldx = X.stride(0) if rows > 1 else kb
     ld = _row_len(kb, fmt)
     cap = _plane_cap(rows, _row_bytes(ld, fmt), predict_slice_count(params) or 1)

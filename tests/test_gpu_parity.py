@@ -323,3 +323,91 @@ def test_fixed_step_split_bitwise(cuda, fmt, emu):
         assert np.array_equal(ss.expo[p], expo[p]), p
     rec = sum(np.ldexp(coeff[p], expo[p][:, None]) for p in range(s))
     assert np.array_equal(bits(rec), bits(X))
+
+
+def _fixed_split_pair(torch, X, fmt, emu, max_planes, cols):
+    """Split X's rows (cols=False) or the columns of X^T given as a transpose
+    view (cols=True) with the fixed-step split and a plane limit."""
+    from paper_2508_00441_b200.slicing import split_many_device, split_deferred
+
+    oz = _oz()
+    f = oz.get_format(fmt)
+    params = oz.compute_params(53, f.mant_bits, 24, X.shape[1])
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    view = Xd.t().contiguous().t() if cols else Xd  # cols: same values, column-major storage
+    (ds,), flags = split_many_device([view], f, params, emu, fixed=True, max_planes=max_planes)
+    dd = split_deferred(view, f, params, emu, fixed=True, max_planes=max_planes)
+    return ds, dd, flags, params
+
+
+@pytest.mark.parametrize("fmt", ["fp8e4m3", "fp16", "fp6e3m2"])
+@pytest.mark.parametrize("emu", [False, True])
+@pytest.mark.parametrize("max_planes", [1, 5, 12, 40])
+def test_fixed_split_plane_limit_rows_and_cols(cuda, fmt, emu, max_planes):
+    """Fixed-step split with a plane limit (the barrier-free row path and the
+    in-place column path, oz_split_fixed_cols): planes, exponents, counts and s
+    equal the CPU restatement, for rows and for columns read in place, through
+    both the synchronous and the deferred (sync-free) split."""
+    import oracle
+
+    torch = cuda
+    rng = np.random.default_rng(77 + max_planes)
+    X = spread_matrix(rng, 70, 1100, 3.0)
+    X[5] = 0.0
+    X[7, :] = 1.0            # ends after one slice
+    X[9, 3] = 2.0 ** -1000   # tiny input: checked slicing
+    X[11, :] *= 2.0 ** 600
+    coeff, expo, cnt, s = oracle.split_rows_fixed(X, _oz().compute_params(53, _oz().get_format(fmt).mant_bits, 24,
+                                                                          X.shape[1]).rho, max_planes)
+    for cols in (False, True):
+        ds, dd, flags, params = _fixed_split_pair(torch, X, fmt, emu, max_planes, cols)
+        assert flags == 0
+        assert ds.s == s, (cols, ds.s, s)
+        assert np.array_equal(ds.row_cnt.cpu().numpy(), cnt), cols
+        ss = _oz().slicing.device_to_sliceset(ds, "rows", params)
+        for p in range(s):
+            assert np.array_equal(bits(ss.coeff[p]), bits(coeff[p])), (cols, p)
+            assert np.array_equal(ss.expo[p], expo[p]), (cols, p)
+        sf = dd.sf.cpu().tolist()
+        if max_planes > 32:  # deferred: cap = 32 planes, the caller redoes the split
+            assert sf[1] == 256, (cols, sf)
+            continue
+        assert sf[0] == s and sf[1] == 0, (cols, sf)
+        codes_d = dd.codes()[:s].cpu().numpy()
+        assert np.array_equal(codes_d, ds.codes()[:s].cpu().numpy()), cols
+        assert np.array_equal(dd.row_cnt.cpu().numpy(), cnt), cols
+
+
+@pytest.mark.parametrize("emu", [False, True])
+def test_fixed_cols_split_matches_transpose(cuda, emu):
+    """oz_split_fixed_cols on B[lo:hi, j0:j1] (strided, odd sizes, a panel
+    offset) is bitwise the transpose + row split the reference-order path uses."""
+    from paper_2508_00441_b200.slicing import split_many_device, transpose_device
+
+    torch = cuda
+    oz = _oz()
+    rng = np.random.default_rng(5)
+    B = torch.from_numpy(spread_matrix(rng, 777, 301, 2.0)).cuda()
+    Bv = B[33:700, 17:290]
+    f = oz.get_format("fp8e4m3")
+    params = oz.compute_params(53, f.mant_bits, 24, Bv.shape[0])
+    (dc,), fc = split_many_device([Bv.t()], f, params, emu, fixed=True, max_planes=11)
+    (dt,), ft = split_many_device([transpose_device(Bv)], f, params, emu, fixed=True, max_planes=11)
+    assert fc == ft == 0 and dc.s == dt.s
+    assert torch.equal(dc.codes()[:dc.s], dt.codes()[:dt.s])
+    assert torch.equal(dc.expo[:dc.s], dt.expo[:dt.s])
+    assert torch.equal(dc.row_cnt, dt.row_cnt)
+
+
+def test_fixed_cols_split_errors(cuda):
+    """Non-finite and subnormal inputs in a column raise like the reference
+    (ValueError / RangeError) through the in-place column split."""
+    oz = _oz()
+    rng = np.random.default_rng(9)
+    A = spread_matrix(rng, 64, 300, 0.5)
+    for bad, exc in ((np.nan, ValueError), (np.inf, ValueError), (5e-324, oz.RangeError)):
+        B = spread_matrix(rng, 300, 80, 0.5)
+        B[100, 41] = bad
+        cfg = oz.GemmConfig(oz.get_format("fp8e4m3"), oz.get_format("fp32"), pair_cutoff=9, slice_exponents="fixed")
+        with pytest.raises(exc):
+            oz.oz_gemm(A, B, cfg)
