@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--skip-zero-pairs", action="store_true", help="enable (result-neutral) zero-pair skipping")
     ap.add_argument("--slice-exponents", choices=("adaptive", "fixed"), default="adaptive",
                     help="fixed: opt-in fixed-step slices + level-grouped accumulation (not bitwise the reference)")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of the cached CUDA graph")
     ap.add_argument("--no-extras", action="store_true", help="skip accuracy / cuBLAS / CPU-baseline legs")
     ap.add_argument("--cpu-rows", type=int, default=128, help="CPU-baseline sample: rows of C")
     ap.add_argument("--cpu-cols", type=int, default=1024, help="CPU-baseline sample: cols of C")
@@ -302,7 +303,7 @@ def main():
     def step():
         if world > 1:
             grid.distribute_panels(dist, groups, rank, A, B)
-        C, st = oz.oz_gemm_device(A, B, cfg, out=Cbuf)
+        C, st = oz.oz_gemm_device(A, B, cfg, out=Cbuf, graph=not args.no_graph)
         return st
 
     Cbuf = torch.empty((n, n), dtype=torch.float64, device=dev)
@@ -511,15 +512,15 @@ def run_extras(args, torch, oz, A, B, cfg, dev, world=1, C_gpu=None, st_gpu=None
     return out
 
 
-def _time_steps(torch, oz, A, B, cfg, steps):
+def _time_steps(torch, oz, A, B, cfg, steps, graph=True):
     """Device-timed full oz_gemm steps (split + fused pair GEMM) on resident inputs."""
     C = torch.empty((A.shape[0], B.shape[1]), dtype=torch.float64, device=A.device)
-    oz.oz_gemm_device(A, B, cfg, out=C)
+    oz.oz_gemm_device(A, B, cfg, out=C, graph=graph)
     torch.cuda.synchronize()
     e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     e[0].record()
     for _ in range(steps):
-        _, st = oz.oz_gemm_device(A, B, cfg, out=C)
+        _, st = oz.oz_gemm_device(A, B, cfg, out=C, graph=graph)
     e[1].record()
     torch.cuda.synchronize()
     return e[0].elapsed_time(e[1]) / steps, st
@@ -542,7 +543,7 @@ def run_variants(args, torch, oz, A, B, Cdd, d, nz, c_cublas, dev, steps=3):
         return float(np.max(np.abs(X[mask] - ref[mask]) / np.abs(ref[mask])))
 
     def one(name, cfg, A_, B_, dd=None, mask=None, cub=None):
-        ms, st = _time_steps(torch, oz, A_, B_, cfg, steps)
+        ms, st = _time_steps(torch, oz, A_, B_, cfg, steps, graph=not args.no_graph)
         row = {"tflops": flops / (ms / 1e3) / 1e12, "ms": ms, "kernel_ms": st.t_gemm * 1e3,
                "split_ms": st.t_slice * 1e3, "gemm_count": st.gemm_count,
                "gemm_ops": st.gemm_ops, "blocks": len(st.blocks),

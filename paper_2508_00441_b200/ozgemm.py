@@ -33,6 +33,7 @@ Opt-in extensions beyond the reference, all off by default:
 from __future__ import annotations
 
 import os
+from collections import OrderedDict
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -181,7 +182,7 @@ PANEL_MARGIN_BYTES = 6 << 30  # HBM left free when planning panels
 _TOTAL_MEM = {}
 
 
-def _panel_plan(m: int, n: int, kb: int, eb: int, torch) -> tuple[int, int]:
+def _panel_plan(m: int, n: int, kb: int, eb: int, torch, quick_only: bool = False) -> tuple[int, int]:
     """Rows / columns of C handled per pass.  C[I, J] needs only A's row panel I
     and B's column panel J (slicing is row/column-local), so when
     B^T and the slice planes of both operands do not fit next to the caller's
@@ -210,6 +211,8 @@ def _panel_plan(m: int, n: int, kb: int, eb: int, torch) -> tuple[int, int]:
         _TOTAL_MEM[dev] = torch.cuda.get_device_properties(dev).total_memory
     if need(mp, np_) < _TOTAL_MEM[dev] // 4:  # common case: no query, no panels
         return mp, np_
+    if quick_only:
+        return None
     free, _ = torch.cuda.mem_get_info()
     budget = max(free - PANEL_MARGIN_BYTES, 1 << 30)
     # Halve the larger extent, keeping panels multiples of 128 (whole MMA tiles,
@@ -222,7 +225,15 @@ def _panel_plan(m: int, n: int, kb: int, eb: int, torch) -> tuple[int, int]:
     return mp, np_
 
 
-def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_out=None, deferred: bool = True):
+def _panel_quick(m, n, kb, eb, cfg, torch) -> bool:
+    """One pass covers all of C without querying free memory (graphable)."""
+    if "OZ_PANEL_ROWS" in os.environ or "OZ_PANEL_COLS" in os.environ:
+        return False
+    return _panel_plan(m, n, kb, eb, torch, quick_only=True) == (m, n)
+
+
+def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_out=None, deferred: bool = True,
+                   graph: bool = False):
     """C = A @ B for CUDA float64 tensors; returns (C, OzStats).  No host copies
     of operands or result (the timed hot path of bench.py) unless ``host_out`` (a
     pinned CPU float64 tensor) is given: then C is also copied there, band by band
@@ -234,8 +245,31 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
     split flags (checked A before B, block by block, as the reference raises)
     and the GEMM flags are read once at the end.  If a split ran out of
     one-pass planes (rare, very wide exponent ranges) the call is redone with
-    the exact two-pass split (``deferred=False``)."""
+    the exact two-pass split (``deferred=False``).
+
+    ``graph`` (with ``out``, device output, single-panel sizes): the whole
+    enqueue phase (splits, padding, exponent prep, pair GEMM) is captured once
+    per (operand addresses, shapes, strides, config) into a CUDA graph and then
+    replayed — one launch per call instead of ~15 host-issued ones, so the GPU
+    does not idle on Python between kernels.  C, flags and exceptions are the
+    same as the eager path; the phase timings come from event nodes captured
+    in the graph."""
     torch = _lib.require_cuda()
+    if A.ndim != 2 or B.ndim != 2 or A.shape[1] != B.shape[0]:
+        raise DimensionError(f"cannot multiply shapes {tuple(A.shape)} and {tuple(B.shape)}")
+    if (graph and out is not None and deferred and host_out is None and cfg.type2.name not in _FP6
+            and A.shape[0] and B.shape[1] and cfg.k_block <= A.shape[1]):
+        st = _graph_state(torch, A, B, cfg, out)
+        if st is not None:
+            st["graph"].replay()
+            return _collect(torch, A, B, cfg, st, timing=timing, host_out=None)
+    st = _enqueue(torch, A, B, cfg, out, timing, host_out, deferred)
+    return _collect(torch, A, B, cfg, st, timing, host_out)
+
+
+def _enqueue(torch, A, B, cfg, out, timing, host_out, deferred):
+    """Every GPU launch of one oz_gemm_device call, no host synchronisation in
+    deferred mode; returns the device state _collect reads."""
     if A.ndim != 2 or B.ndim != 2 or A.shape[1] != B.shape[0]:
         raise DimensionError(f"cannot multiply shapes {tuple(A.shape)} and {tuple(B.shape)}")
     m, k = A.shape
@@ -252,7 +286,6 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
     lim = [v for v in (cfg.max_slices, None if cfg.pair_cutoff is None else cfg.pair_cutoff + 1) if v]
     max_planes = min(lim) if fixed and lim else 0
     fx = {"fixed": fixed, "max_planes": max_planes}
-    stats = OzStats()
     C = out if out is not None else torch.empty((m, n), dtype=torch.float64, device=A.device)
     sp = _lib.stream_ptr(torch)
     kblocks = _blocks(k, cfg.k_block)
@@ -278,7 +311,9 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
             j1 = min(n, j0 + np_)
             for i0 in range(0, max(m, 1), mp):
                 i1 = min(m, i0 + mp)
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timing else None
+                # external=True: inside a graph capture the records become event
+                # nodes, so every replay re-times its phases
+                ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(3)] if timing else None
                 if timing:
                     ev[0].record()
                 # Row panel of A, column panel of B (columns as K-major rows); B's
@@ -322,6 +357,51 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
             _copy_stream(torch).synchronize()
         else:  # panelled: plain copy after the last panel
             host_out.copy_(C)
+    return {"C": C, "gflags": gflags, "blocks": blocks, "evs": evs, "mp": mp, "np": np_, "deferred": deferred}
+
+
+def _graph_state(torch, A, B, cfg, out):
+    """Cached CUDA graph of _enqueue for these operands (None: not graphable,
+    e.g. panelled sizes).  The graph owns its intermediates (private pool) and
+    its output C unless ``out`` is given."""
+    m, k = A.shape
+    n = B.shape[1]
+    kblocks = _blocks(k, cfg.k_block)
+    eb = _lib.ELEM_BYTES.get(cfg.type2.name, 1)
+    for lo, hi in kblocks:
+        if not _panel_quick(m, n, hi - lo, eb, cfg, torch):
+            return None  # panelled (or near the memory limit): eager path
+    key = (A.data_ptr(), tuple(A.shape), tuple(A.stride()), B.data_ptr(), tuple(B.shape), tuple(B.stride()),
+           None if out is None else (out.data_ptr(), tuple(out.stride())), repr(cfg), torch.cuda.current_device(),
+           PACE_SLACK)
+    st = _GRAPHS.get(key)
+    if st is not None:
+        _GRAPHS.move_to_end(key)
+        return st
+    # Warm-up outside the capture: code tables, tensor-map encoders, kernel
+    # attributes; it also raises the reference's exceptions for bad inputs.
+    oz_gemm_device(A, B, cfg, out=out, timing=False)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g, stream=side):
+            st = _enqueue(torch, A, B, cfg, out, True, None, True)
+    torch.cuda.current_stream().wait_stream(side)
+    st["graph"] = g
+    _GRAPHS[key] = st
+    while len(_GRAPHS) > GRAPH_CACHE:
+        _GRAPHS.popitem(last=False)
+    return st
+
+
+def _collect(torch, A, B, cfg, st, timing, host_out):
+    """The one synchronisation: split counts and flags (deferred mode) and the
+    GEMM flags; raises in the reference's order, builds OzStats."""
+    m, k = A.shape
+    n = B.shape[1]
+    C, gflags, blocks, evs, mp, np_ = st["C"], st["gflags"], st["blocks"], st["evs"], st["mp"], st["np"]
+    stats = OzStats()
     # The one synchronisation: split counts / flags (deferred mode) + GEMM flags.
     words = [gflags] + [t for b in blocks for t in b[3] + b[4]]
     host = torch.cat(words).cpu().tolist()
@@ -357,6 +437,10 @@ def oz_gemm_device(A, B, cfg: GemmConfig, out=None, timing: bool = True, host_ou
         stats.t_slice = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3
         stats.t_gemm = sum(e[1].elapsed_time(e[2]) for e in evs) / 1e3
     return C, stats
+
+
+_GRAPHS = OrderedDict()
+GRAPH_CACHE = int(os.environ.get("OZ_GRAPH_CACHE", "2"))  # cached graphs (each holds its slice planes)
 
 
 _COPY_STREAMS = {}

@@ -411,3 +411,32 @@ def test_fixed_cols_split_errors(cuda):
         cfg = oz.GemmConfig(oz.get_format("fp8e4m3"), oz.get_format("fp32"), pair_cutoff=9, slice_exponents="fixed")
         with pytest.raises(exc):
             oz.oz_gemm(A, B, cfg)
+
+
+@pytest.mark.parametrize("kw", [{}, {"pair_cutoff": 9, "slice_exponents": "fixed"}, {"k_block": 256},
+                                {"fp64_emulation": True}, {"type2": "fp16", "k_block": 300}],
+                         ids=["defaults", "fixed9", "kb256", "emu", "fp16kb300"])
+def test_graph_replay_bitwise(cuda, kw):
+    """oz_gemm_device(graph=True): the captured CUDA graph, replayed on new
+    contents of the same operand buffers, gives bitwise the eager C, and a
+    non-finite input written after the capture still raises ValueError."""
+    torch = cuda
+    oz = _oz()
+    kw = dict(kw)
+    t2 = kw.pop("type2", "fp8e4m3")
+    cfg = oz.GemmConfig(oz.get_format(t2), oz.get_format("fp32"), **kw)
+    rng = np.random.default_rng(3)
+    A = torch.from_numpy(spread_matrix(rng, 300, 700, 1.0)).cuda()
+    B = torch.from_numpy(spread_matrix(rng, 700, 260, 1.0)).cuda()
+    Cg = torch.empty((300, 260), dtype=torch.float64, device="cuda")
+    for it in range(3):
+        A.copy_(torch.from_numpy(spread_matrix(rng, 300, 700, 0.5 + it)))
+        B.copy_(torch.from_numpy(spread_matrix(rng, 700, 260, 0.5 + it)))
+        _, sg = oz.oz_gemm_device(A, B, cfg, out=Cg, graph=True)
+        Ce, se = oz.oz_gemm_device(A, B, cfg)
+        assert torch.equal(Cg.view(torch.int64), Ce.view(torch.int64)), it
+        assert [(b.s_x, b.s_y) for b in sg.blocks] == [(b.s_x, b.s_y) for b in se.blocks]
+        assert sg.t_gemm > 0
+    A[5, 7] = float("nan")
+    with pytest.raises(ValueError):
+        oz.oz_gemm_device(A, B, cfg, out=Cg, graph=True)
