@@ -12,9 +12,11 @@ no explicit flush is needed between steps.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-N > 1 (torchrun): 2-D output-tile sharding — each rank owns one n x n tile of
-a (R*n) x (Cc*n) C, its A row-panel and B column-panel broadcast once per step
-over NCCL from the row-/column-group roots (weak scaling: per-GPU work fixed).
+N > 1 (torchrun), and --strong at N = 1: BASELINE config 5 — ONE n x n x n
+DGEMM (n = 65536 unless --n) with C split into 2-D tiles over the ranks
+(1x2, 2x2, 2x4), each rank's A row panel / B column panel broadcast once per
+step over NCCL from the row / column roots, no reduction (strong scaling).
+--weak keeps the old N > 1 mode: one n x n tile per rank (weak scaling).
 --impl reference times the reference algorithm on the host cores (the C
 restatement under oracle/; the reference itself is pure Python/numpy).
 """
@@ -48,7 +50,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--n", "--size", dest="n", type=int, default=None,
+                    help="matrix size (default 8192; 65536 for the strong-scaling config-5 mode)")
+    ap.add_argument("--strong", action="store_true",
+                    help="config 5: one n x n C split into 2-D tiles over the ranks (default when N > 1)")
+    ap.add_argument("--weak", action="store_true", help="N > 1: one n x n tile per rank (weak scaling)")
     ap.add_argument("--phi", type=float, default=0.5)
     ap.add_argument("--type2", default="fp8e4m3")
     ap.add_argument("--type3", default="fp32")
@@ -65,7 +71,12 @@ def parse():
     ap.add_argument("--cpu-cols", type=int, default=1024, help="CPU-baseline sample: cols of C")
     ap.add_argument("--acc-rows", type=int, default=256, help="rows of C checked against the DD oracle")
     ap.add_argument("--no-variants", action="store_true", help="skip the other BASELINE configs (rank 0, N=1)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    a.strong = a.impl == "ours" and (a.strong or (world > 1 and not a.weak))
+    if a.n is None:
+        a.n = 65536 if a.strong else 8192
+    return a
 
 
 def make_inputs(n_rows, n_k, n_cols, phi, seed):
@@ -261,6 +272,9 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.strong:
+        run_strong(args)
+        return
     import torch
     import torch.distributed as dist
 
@@ -403,6 +417,199 @@ def main():
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_strong(args):
+    """BASELINE config 5: ONE n x n x n Ozaki DGEMM (n = 65536 by default) on N
+    GPUs — C split into an R x Cc grid of 2-D tiles (TileGrid: 1x1, 1x2, 2x2,
+    2x4), each rank's A row panel and B column panel distributed once per
+    GEMM by NCCL broadcast from the row / column roots, no reduction.  A step
+    = panel distribution + the rank's tile GEMM (panelled inside a rank when
+    the tile's slice planes do not fit); value = 2 n^3 / max-over-ranks step
+    time (strong scaling: total work fixed)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_00441_b200 as oz
+    from paper_2508_00441_b200.distributed import TileGrid
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    one_gpu = os.environ.get("OZ_BENCH_ONE_GPU") == "1"  # test hook: all ranks on cuda:0, gloo
+    if one_gpu:
+        local = 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("gloo" if one_gpu else "nccl", **({} if one_gpu else {"device_id": dev}))
+    n = args.n
+    cfg = oz.GemmConfig(oz.get_format(args.type2), oz.get_format(args.type3), k_block=args.kblock,
+                        fp64_emulation=args.emu, max_slices=args.max_slices, pair_cutoff=args.pair_cutoff,
+                        skip_zero_pairs=args.skip_zero_pairs, slice_exponents=args.slice_exponents)
+    grid = TileGrid.for_world(world)
+    ti, tj = grid.coords(rank)
+    (r0, r1), (c0, c1) = grid.tile_extent(rank, n, n)
+    groups = grid.make_groups(dist) if world > 1 else None
+    # Panels: the row root generates A[r0:r1, :], the column root B[:, c0:c1]
+    # (same global matrices for every N: generated panel-by-panel from the
+    # global seeds in 8192-row / -column chunks); the others receive them.
+    A = torch.empty((r1 - r0, n), dtype=torch.float64, device=dev)
+    B = torch.empty((n, c1 - c0), dtype=torch.float64, device=dev)
+    if grid.is_row_root(rank):
+        fill_rows(torch, A, r0, n, args.phi, 1000, dev)
+    if grid.is_col_root(rank):
+        fill_cols(torch, B, c0, n, args.phi, 2000, dev)
+    C = torch.empty((r1 - r0, c1 - c0), dtype=torch.float64, device=dev)
+    ev_d = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def step(timing=False):
+        if timing:
+            ev_d[0].record()
+        if world > 1:
+            grid.distribute_panels(dist, groups, rank, A, B)
+        if timing:
+            ev_d[1].record()
+        _, st = oz.oz_gemm_device(A, B, cfg, out=C, graph=not args.no_graph)
+        return st
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    gemm_s, slice_s = [], []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev[0].record()
+        for _ in range(args.steps):
+            st = step(timing=True)
+            gemm_s.append(st.t_gemm)
+            slice_s.append(st.t_slice)
+        ev[1].record()
+        torch.cuda.synchronize()
+    clocks = clk.summary()
+    tot_ms = ev[0].elapsed_time(ev[1])
+    d_ms = ev_d[0].elapsed_time(ev_d[1])  # last step's panel distribution
+    if world > 1:
+        t = torch.tensor([tot_ms, d_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms, d_ms = (float(v) for v in t.tolist())
+    flops = 2.0 * n * n * n
+    value = flops * args.steps / (tot_ms / 1e3) / 1e12
+    blk = st.blocks[0]
+    gemm_ms = statistics.mean(gemm_s) * 1e3
+    tile_mma = 2.0 * (r1 - r0) * (c1 - c0) * n * blk.gemms
+    peaks = measured_peaks()
+    fp8_peak = 2.0 * peaks["bf16"]
+    achieved = tile_mma / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": fp8_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp8_peak if achieved else None, "traffic": None,
+                "kernel": "pair_gemm_kernel (this rank's C tile; all of its panel passes)",
+                "peak_source": f"dense fp8 = 2 x measured dense bf16 ({peaks['source']})",
+                "algorithmic_flops_per_launch": tile_mma, "kernel_ms": gemm_ms,
+                "split_ms": statistics.mean(slice_s) * 1e3}
+    # Bitwise parity sample of this rank's tile (rank 0): the oracle on a few
+    # of its A rows and B columns at the full inner dimension n.
+    parity = None
+    if rank == 0 and not args.no_extras:
+        import oracle
+
+        rows = sample_index(r1 - r0, 16, 2)
+        cols = sample_index(c1 - c0, 64, 4)
+        ri, ci = torch.from_numpy(rows).to(dev), torch.from_numpy(cols).to(dev)
+        As, Bs = A.index_select(0, ri).cpu().numpy(), B.index_select(1, ci).cpu().numpy()
+        Cs = C.index_select(0, ri).index_select(1, ci).cpu().numpy()
+        if args.slice_exponents == "fixed":
+            Cref, _ = oracle.oz_gemm_fixed(As, Bs, args.type2, args.type3, args.kblock, args.max_slices,
+                                           "smallest-first", args.pair_cutoff,
+                                           pad_to=[(b.s_x, b.s_y) for b in st.blocks])
+            fl = 0
+        else:
+            Cref, info = oracle.oz_gemm(As, Bs, args.type2, args.type3, args.kblock, args.emu, args.max_slices,
+                                        "smallest-first", args.pair_cutoff, nthreads=oracle.max_threads())
+            fl = info["flags"]
+        nbad = int(np.sum(Cs.view(np.uint64) != Cref.view(np.uint64)))
+        parity = {"sample": f"C[{len(rows)}x{len(cols)}] of rank 0's tile (global rows {r0}+, cols {c0}+), "
+                            f"oracle on the same A rows / B columns at k={n}",
+                  "entries": int(Cs.size), "mismatches": nbad, "bitwise_equal": nbad == 0 and fl == 0}
+    # e2e: host panels in (pinned; the roots copy theirs to the device, then the
+    # broadcast), host C tiles out; one step, max over ranks.
+    e2e = None
+    if not args.no_extras:
+        Ah = A.cpu().pin_memory() if grid.is_row_root(rank) else None
+        Bh = B.cpu().pin_memory() if grid.is_col_root(rank) else None
+        Ch = torch.empty(C.shape, dtype=torch.float64, pin_memory=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if Ah is not None:
+            A.copy_(Ah, non_blocking=True)
+        if Bh is not None:
+            B.copy_(Bh, non_blocking=True)
+        step()
+        Ch.copy_(C, non_blocking=True)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        h2d = (Ah.numel() * 8 if Ah is not None else 0) + (Bh.numel() * 8 if Bh is not None else 0)
+        if world > 1:
+            t = torch.tensor([dt, h2d], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t[0].item())
+            t = torch.tensor([h2d], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            h2d = int(t.item())
+        e2e = {"value": flops / dt / 1e12, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": 8 * n * n,
+               "path": "root ranks: pinned host panels -> device, NCCL panel broadcast, tile GEMM, "
+                       "every rank: C tile -> pinned host (max over ranks)"}
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None,
+               "dtype": f"f64 ({args.type2} slice products)",
+               "data": "synthetic (rand-0.5)*exp(phi*randn), generated on the panel roots' devices",
+               "config": dict(workload_config(args), parallelism=f"2-D C tiles {grid.rows}x{grid.cols}",
+                              tile=[r1 - r0, c1 - c0]),
+               "e2e": e2e, "gpu_launches": KERNELS_PER_BLOCK * len(st.blocks) * args.steps,
+               "roofline": roofline, "clocks": clocks,
+               "distribution_ms": d_ms,
+               "distribution": f"NCCL broadcast of A row panels in row groups and B column panels in column "
+                               f"groups, once per step (max over ranks, {d_ms:.1f} ms of the step)",
+               "slices": {"s_x": blk.s_x, "s_y": blk.s_y, "gemm_count": st.gemm_count},
+               "parity": parity}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def fill_rows(torch, A, r0, n, phi, seed, dev, chunk=8192):
+    """A[:, :] = rows r0.. of the global A (generated in fixed 8192-row chunks
+    seeded by chunk index, so every N sees the same global matrix)."""
+    rows = A.shape[0]
+    for g0 in range(r0 // chunk * chunk, r0 + rows, chunk):
+        blk = gpu_rows(torch, min(chunk, n - g0), n, phi, seed * 100003 + g0 // chunk, dev)
+        lo, hi = max(g0, r0), min(g0 + chunk, r0 + rows)
+        A[lo - r0:hi - r0].copy_(blk[lo - g0:hi - g0])
+        del blk
+
+
+def fill_cols(torch, B, c0, n, phi, seed, dev, chunk=8192):
+    """B[:, :] = columns c0.. of the global B (chunks of 8192 columns)."""
+    cols = B.shape[1]
+    for g0 in range(c0 // chunk * chunk, c0 + cols, chunk):
+        blk = gpu_rows(torch, min(chunk, n - g0), n, phi, seed * 100003 + g0 // chunk, dev)  # chunk^T
+        lo, hi = max(g0, c0), min(g0 + chunk, c0 + cols)
+        B[:, lo - c0:hi - c0].copy_(blk[lo - g0:hi - g0].t())
+        del blk
+
+
+def gpu_rows(torch, rows, cols, phi, seed, dev):
+    g = torch.Generator(device=dev).manual_seed(seed)
+    return (torch.rand((rows, cols), generator=g, device=dev, dtype=torch.float64) - 0.5) * torch.exp(
+        phi * torch.randn((rows, cols), generator=g, device=dev, dtype=torch.float64))
 
 
 def fp64_level_summary(extras):

@@ -138,10 +138,10 @@ int oz_tile_counts(const int32_t* row_cnt, int64_t rows, int32_t* tile_cnt, void
  *   (opt-in extension).  emu: integer-only FP64 epilogue.  accumulate: 0 writes
  *   C = Cb, 1 writes C = C + Cb.
  *   workspace / workspace_bytes: device scratch of at least
- *   oz_pair_gemm_workspace(m, n, sx, sy, pair_cutoff) bytes (per-tile B
+ *   oz_pair_gemm_workspace(m, n, kb, type2, sx, sy, pair_cutoff) bytes (per-tile B
  *   exponents for the epilogue, then the pacing counters); OZ_EINVAL if smaller
  *   than the exponent part.  pace_slack > 0 enables cross-CTA pacing — resident
- *   CTAs stay within pace_slack pair-steps of each other so slice panels are
+ *   CTAs stay within pace_slack steps (8192-element K chunks of a pair) of each other so slice panels are
  *   reused from L2 (scheduling only; results are identical); ignored when
  *   tile_cnt_a != NULL or the workspace has no room for the counters.
  *   C_host / ldc_host / copy_stream: optional device->host copy of the finished
@@ -177,7 +177,7 @@ int oz_pair_gemm_grouped(const void* a_planes, const void* b_planes, int64_t ld_
 
 /* Bytes of device workspace oz_pair_gemm needs for these sizes (0 if there is
  * nothing to compute). */
-int64_t oz_pair_gemm_workspace(int64_t m, int64_t n, int sx, int sy, int pair_cutoff);
+int64_t oz_pair_gemm_workspace(int64_t m, int64_t n, int64_t kb, int type2, int sx, int sy, int pair_cutoff);
 
 /* Tuning override of oz_pair_gemm's kernel variant (no reference counterpart;
  * results are bitwise identical in every variant): cta_group 1 | 2, tile_n

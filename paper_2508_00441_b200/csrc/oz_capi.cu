@@ -242,7 +242,7 @@ struct PairPlan {
 // once by experiments and the variant tests — never read from the environment.
 std::atomic<int> g_force_cta{0}, g_force_tn{0}, g_force_group{0};
 
-PairPlan plan_pair(int64_t m, int64_t n, int sx, int sy, int pair_cutoff, int emu) {
+PairPlan plan_pair(int64_t m, int64_t n, int64_t kb, int elem_bytes, int sx, int sy, int pair_cutoff, int emu) {
   PairPlan pl{};
   // CTA pair (cta_group::2) unless the problem has a single 128-row slab; N = 192
   // columns per pair tile in hardware-FP64 mode (tensor-bound), N = 128 in the
@@ -270,7 +270,8 @@ PairPlan plan_pair(int64_t m, int64_t n, int sx, int sy, int pair_cutoff, int em
       if (pair_cutoff < 0 || p + q <= pair_cutoff) ++pl.pairs;
   const size_t n_pad = (size_t)pl.tiles_n * pl.tn;
   pl.eb_bytes = (sizeof(int32_t) * (size_t)sy * (n_pad + 2 * (size_t)pl.tiles_n) + 255) / 256 * 256;
-  pl.pace_bytes = sizeof(uint32_t) * (size_t)pl.tiles_m * pl.tiles_n * (size_t)pl.pairs;
+  const int64_t num_kb = (kb * elem_bytes + 127) / 128, spp = (num_kb + oz::kPaceBlocks - 1) / oz::kPaceBlocks;
+  pl.pace_bytes = sizeof(uint32_t) * (size_t)pl.tiles_m * pl.tiles_n * (size_t)pl.pairs * (size_t)spp;
   pl.group = 8;
   if (const int f = g_force_group.load(std::memory_order_relaxed)) pl.group = f;
   pl.bands = (pl.tiles_m + pl.group - 1) / pl.group;
@@ -294,9 +295,13 @@ int split_impl(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2
 
 extern "C" {
 
-int64_t oz_pair_gemm_workspace(int64_t m, int64_t n, int sx, int sy, int pair_cutoff) {
-  if (m <= 0 || n <= 0 || sx <= 0 || sy <= 0) return 0;
-  const PairPlan p0 = plan_pair(m, n, sx, sy, pair_cutoff, 0), p1 = plan_pair(m, n, sx, sy, pair_cutoff, 1);
+int64_t oz_pair_gemm_workspace(int64_t m, int64_t n, int64_t kb, int type2, int sx, int sy, int pair_cutoff) {
+  if (m <= 0 || n <= 0 || kb <= 0 || sx <= 0 || sy <= 0) return 0;
+  LpFormat f;
+  uint32_t idf;
+  if (!fmt_info(type2, f, idf)) return 0;
+  const PairPlan p0 = plan_pair(m, n, kb, f.bytes, sx, sy, pair_cutoff, 0),
+                 p1 = plan_pair(m, n, kb, f.bytes, sx, sy, pair_cutoff, 1);
   const size_t b0 = p0.eb_bytes + p0.band_bytes + p0.pace_bytes, b1 = p1.eb_bytes + p1.band_bytes + p1.pace_bytes;
   return (int64_t)(b0 > b1 ? b0 : b1);
 }
@@ -509,7 +514,7 @@ static int pair_gemm_impl(const void* a_planes, const void* b_planes, int64_t ld
   P.order = order; P.cutoff = pair_cutoff; P.accumulate = accumulate;
   P.elem_bytes = f.bytes; P.fmt = idf; P.flags = flags; P.s_dev = s_dev;
   P.fp6 = (type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3) ? 1 : 0;
-  const PairPlan pl = plan_pair(m, n, sx, sy, pair_cutoff, emu);
+  const PairPlan pl = plan_pair(m, n, kb, f.bytes, sx, sy, pair_cutoff, emu);
   const int cta = pl.cta, tn = pl.tn;
   if (!workspace || (size_t)workspace_bytes < pl.eb_bytes) return OZ_EINVAL;  // see oz_pair_gemm_workspace
   P.group = pl.group;

@@ -25,8 +25,9 @@
 //               reference pair order, with __dadd_rn (HW mode) or the integer-only
 //               add (EMU mode — no DADD/DMUL/DFMA in that instantiation,
 //               tests/test_capi.py checks the SASS).
-// Producers of all resident CTAs are paced to within `pace_slack` pair-steps of
-// each other so concurrently used slice panels stay L2-resident.
+// Producers of all resident CTAs are paced to within `pace_slack` steps (a pair's
+// k-blocks in chunks of kPaceBlocks) of each other so concurrently used slice
+// panels stay L2-resident.
 // Performance note: DADDs only drain while the MMA warp waits for
 // an accumulator, so the epilogue work after a pair's first DADD is exposed.
 #ifndef OZ_TERM_FMA
@@ -46,6 +47,7 @@ constexpr int kPM = 128;                   // per-CTA output rows
 constexpr int kEpiWarps = 8;
 constexpr int kPThreads = 128 + 32 * kEpiWarps;
 constexpr int kTmemCols = 512;             // whole TMEM: accumulators (+ part of Cb for N > 128)
+constexpr int kPaceBlocks = 64;            // k-blocks per cross-CTA pacing step (8192 FP8 / 4096 FP16 K)
 
 // kN = output columns per CTA (and MMA N).  Hardware-FP64 mode: N = 128 keeps Cb
 // fully in registers with 4 TMEM accumulators; N = 192 (cta_group::2 only) has 2
@@ -101,8 +103,9 @@ struct PairParams {
   uint32_t fmt;              // idesc a/b format code
   uint32_t* flags;
   // Cross-CTA pacing (L2 locality): producers of all resident CTAs stay within
-  // `pace_slack` pair-steps of each other.  step_ctr has waves*pairs_per_tile
-  // zeroed counters; nullptr disables pacing (required when tiles skip pairs).
+  // `pace_slack` steps of each other (a step = kPaceBlocks k-blocks of one pair).
+  // step_ctr has waves*pairs_per_tile*ceil(num_kb/kPaceBlocks) zeroed counters;
+  // nullptr disables pacing (required when tiles skip pairs).
   uint32_t* step_ctr;
   int pace_slack;
   int pairs_per_tile;
@@ -549,6 +552,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const int unit = blockIdx.x / kCta, num_units = gridDim.x / kCta;  // tile-processing unit (CTA or pair)
   constexpr int kb_elems = 128 / kElemBytes;
   const int num_kb = (P.kb + kb_elems - 1) / kb_elems;
+  const int spp = (num_kb + kPaceBlocks - 1) / kPaceBlocks;  // pacing steps per pair
+  const int steps_per_tile = pairs_per_tile * spp;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&map_a);
@@ -587,25 +592,28 @@ __global__ void __launch_bounds__(kPThreads, 1)
           int t = 0;
           for (pi.init(lp, lq, P.order, P.cutoff); pi.valid(); pi.next(), ++t) {
             const int p = pi.p, q = pi.q();
-            if (P.step_ctr && pacing) {
-              // Wait until every CTA of the wave `pace_slack` steps back has issued its loads.
-              // Scheduling only: if that takes implausibly long (CTAs not co-resident),
-              // stop pacing instead of risking a deadlock.
-              const int g = wave * pairs_per_tile + t - P.pace_slack;
-              if (g >= 0) {
-                const int gw = g / pairs_per_tile;
-                const uint32_t need = (uint32_t)(kCta * min(num_units, num_tiles - gw * num_units));
-                const long long t0 = clock64();
-                while (ld_relaxed_gpu(P.step_ctr + g) < need) {
-                  __nanosleep(32);
-                  if (clock64() - t0 > (1ll << 26)) {
-                    pacing = false;
-                    break;
+            for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
+              // Pacing steps: chunks of kPaceBlocks k-blocks of a pair (one step per pair
+              // for kb <= 8192 FP8), so long inner dimensions stay L2-local too.
+              const int u = t * spp + kbi / kPaceBlocks;  // this tile's step index
+              if (P.step_ctr && pacing && kbi % kPaceBlocks == 0) {
+                // Wait until every CTA of the wave `pace_slack` steps back has issued its loads.
+                // Scheduling only: if that takes implausibly long (CTAs not co-resident),
+                // stop pacing instead of risking a deadlock.
+                const int g = wave * steps_per_tile + u - P.pace_slack;
+                if (g >= 0) {
+                  const int gw = g / steps_per_tile;
+                  const uint32_t need = (uint32_t)(kCta * min(num_units, num_tiles - gw * num_units));
+                  const long long t0 = clock64();
+                  while (ld_relaxed_gpu(P.step_ctr + g) < need) {
+                    __nanosleep(32);
+                    if (clock64() - t0 > (1ll << 26)) {
+                      pacing = false;
+                      break;
+                    }
                   }
                 }
               }
-            }
-            for (int kbi = 0; kbi < num_kb; ++kbi, ++it) {
               const uint32_t st = it % kStages;
               if (it >= (uint32_t)kStages) mbar_wait(&s.empty[st], ((it / kStages) - 1) & 1);
               if constexpr (kCta == 1) {
@@ -618,8 +626,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 tma_load_3d_pair(s.a[st], &map_a, &s.full[st], kbi * kb_elems, arow, p, P.hint_a);
                 tma_load_3d_pair(s.b[st], &map_b, &s.full[st], kbi * kb_elems, brow, q, P.hint_b);
               }
+              if (P.step_ctr && (kbi % kPaceBlocks == kPaceBlocks - 1 || kbi == num_kb - 1))
+                red_relaxed_gpu_add(P.step_ctr + wave * steps_per_tile + u, 1u);
             }
-            if (P.step_ctr) red_relaxed_gpu_add(P.step_ctr + wave * pairs_per_tile + t, 1u);
           }
         }
       }

@@ -350,7 +350,10 @@ def _enqueue(torch, A, B, cfg, out, timing, host_out, deferred):
                 if timing:
                     ev[2].record()
                     evs.append(ev)
-            del Bt, sb
+                # Release this panel's planes before the next panel allocates its own
+                # (stream-ordered reuse; otherwise two panels' planes peak together).
+                sa = None
+            Bt = sb = None
         blocks.append((lo, hi, kb, sfa, sfb, s_a, s_b, hfa, hfb))
     if host_out is not None:
         if mp == m and np_ == n and m and n:
@@ -474,7 +477,8 @@ def _pair_pass(torch, cfg, sa, sb, m, n, kb, order, cutoff, emu, bi, C, i0, j0, 
         tcb = torch.empty((n + 127) // 128, dtype=torch.int32, device=C.device)
         _lib.call("oz_tile_counts", sa.row_cnt.data_ptr(), m, tca.data_ptr(), sp)
         _lib.call("oz_tile_counts", sb.row_cnt.data_ptr(), n, tcb.data_ptr(), sp)
-    ws_bytes = _lib.load().oz_pair_gemm_workspace(m, n, sx, sy, cutoff) if m and n and sx and sy else 0
+    ws_bytes = _lib.load().oz_pair_gemm_workspace(m, n, kb, _lib.FMT_CODE[cfg.type2.name], sx, sy, cutoff) \
+        if m and n and sx and sy else 0
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=C.device)
     if host:
         # The copy stream waits on the band counters inside ws and reads C: keep

@@ -124,7 +124,7 @@ def test_hw_kernels_do_use_fp64_and_tensor_cores(lib):
 
 def test_pair_gemm_workspace_query_without_gpu(lib):
     # pure host arithmetic: exponent table + pacing counters, 0 when nothing to do
-    assert lib.oz_pair_gemm_workspace(0, 128, 3, 3, -1) == 0
-    small = lib.oz_pair_gemm_workspace(256, 192, 4, 4, -1)
+    assert lib.oz_pair_gemm_workspace(0, 128, 256, 0, 3, 3, -1) == 0
+    small = lib.oz_pair_gemm_workspace(256, 192, 256, 0, 4, 4, -1)
     assert small > 0 and small % 4 == 0
-    assert lib.oz_pair_gemm_workspace(8192, 8192, 16, 17, -1) > lib.oz_pair_gemm_workspace(8192, 8192, 16, 17, 11)
+    assert lib.oz_pair_gemm_workspace(8192, 8192, 8192, 0, 16, 17, -1) > lib.oz_pair_gemm_workspace(8192, 8192, 8192, 0, 16, 17, 11)
