@@ -41,8 +41,8 @@ import numpy as np
 from . import _lib
 from .errors import DimensionError, SlicingInfeasible
 from .formats import FormatSpec
-from .slicing import (compute_params, predict_gemm_count, predict_slice_count, split_deferred, split_many_device,
-                      transpose_device)
+from .slicing import (Arena, compute_params, predict_gemm_count, predict_slice_count, split_deferred,
+                      split_many_device, transpose_device)
 
 __all__ = [
     "DimensionError", "GemmConfig", "BlockStats", "OzStats", "OzResult", "transpose", "oz_gemm",
@@ -214,6 +214,8 @@ def _panel_plan(m: int, n: int, kb: int, eb: int, torch, quick_only: bool = Fals
     if quick_only:
         return None
     free, _ = torch.cuda.mem_get_info()
+    # Blocks torch's caching allocator holds but has not handed out are free to us too.
+    free += torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
     budget = max(free - PANEL_MARGIN_BYTES, 1 << 30)
     # Halve the larger extent, keeping panels multiples of 128 (whole MMA tiles,
     # and 16-byte aligned C column offsets for the vectorised epilogue stores).
@@ -304,6 +306,8 @@ def _enqueue(torch, A, B, cfg, out, timing, host_out, deferred):
                 f"slice width {params.slice_width} < 0 for m2={params.m2}, m3={params.m3}, k={kb}")
         _check_accumulator(params, kb)
         mp, np_ = _panel_plan(m, n, kb, eb, torch) if m and n else (max(m, 1), max(n, 1))
+        # Panelled: every pass reuses one set of plane / transpose buffers.
+        arena = Arena(torch, A.device) if (mp < m or np_ < n) and deferred else None
         s_a = s_b = 0
         sfa, sfb = [], []
         hfa, hfb = [], []  # non-deferred: host flag words of the splits
@@ -319,11 +323,11 @@ def _enqueue(torch, A, B, cfg, out, timing, host_out, deferred):
                 # Row panel of A, column panel of B (columns as K-major rows); B's
                 # panel is sliced once per column panel (j0 loop outside).
                 if deferred:
-                    sa = split_deferred(A[i0:i1, lo:hi], cfg.type2, params, emu, **fx)
+                    sa = split_deferred(A[i0:i1, lo:hi], cfg.type2, params, emu, arena=arena, slot="A", **fx)
                     sfa.append(sa.sf)
                     if i0 == 0:
-                        Bt = _b_cols(B[lo:hi, j0:j1], fixed and max_planes > 0)
-                        sb = split_deferred(Bt, cfg.type2, params, emu, **fx)
+                        Bt = _b_cols(B[lo:hi, j0:j1], fixed and max_planes > 0, arena)
+                        sb = split_deferred(Bt, cfg.type2, params, emu, arena=arena, slot="B", **fx)
                         sfb.append(sb.sf)
                     s_dev = torch.cat([sa.sf[:1], sb.sf[:1]])
                 else:
@@ -450,11 +454,11 @@ _COPY_STREAMS = {}
 _FP6 = ("fp6e3m2", "fp6e2m3")
 
 
-def _b_cols(Bv, in_place: bool):
+def _b_cols(Bv, in_place: bool, arena=None):
     """B's column panel with columns as K-major rows: a transpose VIEW when the
     fixed-step split reads columns in place (oz_split_fixed_cols), else the
     device transpose (slicing.py:199-203 slices columns via the transpose)."""
-    return Bv.t() if in_place and (Bv.stride(1) == 1 or Bv.shape[1] == 1) else transpose_device(Bv)
+    return Bv.t() if in_place and (Bv.stride(1) == 1 or Bv.shape[1] == 1) else transpose_device(Bv, arena)
 
 
 def _copy_stream(torch):

@@ -321,13 +321,36 @@ def split_many_device(Xs, fmt: FormatSpec, params: SlicingParams, emu: bool, str
     return out, all_flags
 
 
+class Arena:
+    """Named flat device buffers reused across the passes of one panelled
+    oz_gemm call (all on one stream, so a pass's reuse is ordered after the
+    previous pass's GEMM): without it every panel allocates ~GiB-sized plane
+    buffers while the previous ones are being freed, and near the memory limit
+    the caching allocator falls back to synchronous cudaFree / cudaMalloc."""
+
+    def __init__(self, torch, device):
+        self.torch, self.device, self.bufs = torch, device, {}
+
+    def take(self, name: str, shape, dtype):
+        n = 1
+        for d in shape:
+            n *= int(d)
+        nbytes = max(n * self.torch.empty((), dtype=dtype).element_size(), 1)
+        buf = self.bufs.get(name)
+        if buf is None or buf.numel() < nbytes:
+            self.bufs.pop(name, None)
+            buf = self.bufs[name] = self.torch.empty(nbytes, dtype=self.torch.uint8, device=self.device)
+        return buf[:nbytes].view(dtype).view(*shape) if n else buf[:0].view(dtype).view(*shape)
+
+
 def split_deferred(X, fmt: FormatSpec, params: SlicingParams, emu: bool, stream=None, fixed: bool = False,
-                   max_planes: int = 0) -> DeviceSlices:
+                   max_planes: int = 0, arena: Arena | None = None, slot: str = "") -> DeviceSlices:
     """One-pass split without a host synchronisation: the fused split and the
     zero padding (which reads s on the device) are only enqueued.  The result
     holds ``cap`` planes; the pair GEMM takes the true s from ``sf`` on the
     device.  The caller reads ``sf`` later and must redo the work with
-    ``split_many_device`` if its flags carry ``FLAG_PLANE_CAP``."""
+    ``split_many_device`` if its flags carry ``FLAG_PLANE_CAP``.  ``arena`` /
+    ``slot``: take the planes, exponents and counts from reused buffers."""
     torch = _lib.require_cuda()
     code = _fmt_code(fmt)
     sp = stream if stream is not None else _lib.stream_ptr(torch)
@@ -339,10 +362,15 @@ def split_deferred(X, fmt: FormatSpec, params: SlicingParams, emu: bool, stream=
     cap = _plane_cap(rows, _row_bytes(ld, fmt), predict_slice_count(params) or 1)
     if fixed and max_planes > 0:
         cap = min(cap, max_planes)
-    sf = torch.zeros(2, dtype=torch.int32, device=X.device)
-    row_cnt = torch.empty(max(rows, 1), dtype=torch.int32, device=X.device)
-    planes = torch.empty((cap, rows, _row_bytes(ld, fmt)), dtype=torch.uint8, device=X.device)
-    expo = torch.empty((cap, rows), dtype=torch.int32, device=X.device)
+    sf = torch.zeros(2, dtype=torch.int32, device=X.device)  # read at the end: never shared
+    if arena is not None:
+        row_cnt = arena.take(slot + "cnt", (max(rows, 1),), torch.int32)
+        planes = arena.take(slot + "planes", (cap, rows, _row_bytes(ld, fmt)), torch.uint8)
+        expo = arena.take(slot + "expo", (cap, rows), torch.int32)
+    else:
+        row_cnt = torch.empty(max(rows, 1), dtype=torch.int32, device=X.device)
+        planes = torch.empty((cap, rows, _row_bytes(ld, fmt)), dtype=torch.uint8, device=X.device)
+        expo = torch.empty((cap, rows), dtype=torch.int32, device=X.device)
     if rows > 0:
         _split_launch(fixed, max_planes, X, rows, kb, ldx, code, params.rho, emu, cap, planes.data_ptr(), ld,
                       expo.data_ptr(), row_cnt, sf.data_ptr(), sf.data_ptr() + 4, sp)
@@ -360,13 +388,14 @@ def _to_device_f64(M):
     return t.contiguous()
 
 
-def transpose_device(X):
+def transpose_device(X, arena: Arena | None = None):
     """Device transpose (kernel ``oz_transpose``) of a 2-D float64 CUDA tensor."""
     torch = _lib.require_cuda()
     rows, cols = X.shape
     if X.stride(1) != 1:
         X = X.contiguous()
-    out = torch.empty((cols, rows), dtype=torch.float64, device=X.device)
+    out = arena.take("Bt", (cols, rows), torch.float64) if arena is not None else \
+        torch.empty((cols, rows), dtype=torch.float64, device=X.device)
     if rows and cols:
         _lib.call("oz_transpose", X.data_ptr(), rows, cols, X.stride(0) if rows > 1 else cols,
                   out.data_ptr(), rows, _lib.stream_ptr(torch))
