@@ -185,6 +185,13 @@ int64_t oz_pair_gemm_workspace(int64_t m, int64_t n, int64_t kb, int type2, int 
  * default).  Process-wide; used by the variant tests and experiments. */
 int oz_set_pair_variant(int cta_group, int tile_n, int raster_group);
 
+/* Tuning knob (results are identical): epilogue warps of the CTA-pair N = 192
+ * hardware-FP64 pair-GEMM kernel — 8 (default; two threads per C row, a third
+ * of Cb in TMEM) or 12 (three threads per row, 48 register + 16 TMEM columns
+ * each; 128 registers per thread spill — measured 5-10% slower,
+ * profiles/epi12_ab_r02.txt). */
+int oz_set_epilogue_warps(int warps);
+
 /* One slice-pair product D (m x n, fp32) = A (m x k) . B (n x k)^T on tcgen05 —
  * replaces lpgemm.lp_gemm (lpgemm.py:93-120) for slice operands (exact). */
 int oz_lp_gemm(const void* a_plane, const void* b_plane, int64_t ld_a, int64_t ld_b, int64_t m, int64_t n,

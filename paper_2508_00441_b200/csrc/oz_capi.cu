@@ -106,13 +106,13 @@ int launch_status() {
   return OZ_OK;
 }
 
-template <bool kEmu, int kCta, int kEB, int kN>
+template <bool kEmu, int kCta, int kEB, int kN, int kEpi = oz::kEpiWarps>
 int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const oz::PairParams& P, int tiles, cudaStream_t st) {
   const size_t smem = oz::pair_gemm_smem_bytes<kCta, kN, kEmu>();
-  auto kern = oz::pair_gemm_kernel<kEmu, kCta, kEB, kN>;
+  auto kern = oz::pair_gemm_kernel<kEmu, kCta, kEB, kN, kEpi>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg{};
-  cfg.blockDim = dim3(oz::kPThreads);
+  cfg.blockDim = dim3(oz::PairCfg<kCta, kN, kEmu, kEpi>::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -140,11 +140,11 @@ int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const oz::PairPara
   return launch_status();
 }
 
-template <bool kEmu, int kCta, int kN>
+template <bool kEmu, int kCta, int kN, int kEpi = oz::kEpiWarps>
 int launch_pair_fmt(const CUtensorMap& ma, const CUtensorMap& mb, const oz::PairParams& P, int tiles,
                     cudaStream_t st) {
-  return P.elem_bytes == 1 ? launch_pair<kEmu, kCta, 1, kN>(ma, mb, P, tiles, st)
-                           : launch_pair<kEmu, kCta, 2, kN>(ma, mb, P, tiles, st);
+  return P.elem_bytes == 1 ? launch_pair<kEmu, kCta, 1, kN, kEpi>(ma, mb, P, tiles, st)
+                           : launch_pair<kEmu, kCta, 2, kN, kEpi>(ma, mb, P, tiles, st);
 }
 
 // Code tables for the fused split, one per (format, rho), built on first use
@@ -241,6 +241,8 @@ struct PairPlan {
 // Tuning overrides (oz_set_pair_variant; 0 = automatic).  Process-wide, set
 // once by experiments and the variant tests — never read from the environment.
 std::atomic<int> g_force_cta{0}, g_force_tn{0}, g_force_group{0};
+// Epilogue warps of the CTA-pair N = 192 hardware-mode kernel (8 or 12).
+std::atomic<int> g_epi_warps{8};
 
 PairPlan plan_pair(int64_t m, int64_t n, int64_t kb, int elem_bytes, int sx, int sy, int pair_cutoff, int emu) {
   PairPlan pl{};
@@ -250,7 +252,8 @@ PairPlan plan_pair(int64_t m, int64_t n, int64_t kb, int elem_bytes, int sx, int
   // of Cb sits in registers; measured 144 -> 109 ms at n = 8192, pair_cutoff = 11).
   // oz_set_pair_variant(cta_group, tile_n, group) overrides (experiments, tests).
   pl.cta = m > oz::kPM ? 2 : 1;
-  if (const int f = g_force_cta.load(std::memory_order_relaxed)) pl.cta = f == 1 ? 1 : 2;
+  const int force_cta = g_force_cta.load(std::memory_order_relaxed);
+  if (force_cta) pl.cta = force_cta == 1 ? 1 : 2;
   pl.tn = 128;
   if (pl.cta == 2 && n > 128 && !emu) {
     // N = 192 unless tile quantisation favours N = 128: time ~ waves x N / efficiency,
@@ -261,7 +264,24 @@ PairPlan plan_pair(int64_t m, int64_t n, int64_t kb, int elem_bytes, int sx, int
     const int64_t w128 = (tm * ((n + 127) / 128) + units - 1) / units;
     pl.tn = (double)w192 * 192.0 <= (double)w128 * 128.0 * 1.07 ? 192 : 128;
   }
-  if (const int f = g_force_tn.load(std::memory_order_relaxed)) pl.tn = (f == 192 && pl.cta == 2 && !emu) ? 192 : 128;
+  {
+    // Small problems: 128 x 64 single-CTA tiles (every SM busy, half the
+    // epilogue work per CTA and pair) when the CTA-pair tiles leave SMs idle.
+    // Cost ~ waves x per-CTA columns / relative efficiency (N = 64: ~0.85 of N = 128).
+    const int64_t sms = num_sms(), units = sms / pl.cta, rows = (int64_t)oz::kPM * pl.cta;
+    const int64_t t2 = ((m + rows - 1) / rows) * ((n + pl.tn - 1) / pl.tn);
+    const double c2 = (double)((t2 + units - 1) / units) * pl.tn * (pl.tn == 192 ? 1.0 : 1.07);
+    const int64_t t64 = ((m + oz::kPM - 1) / oz::kPM) * ((n + 63) / 64);
+    const double c64 = (double)((t64 + sms - 1) / sms) * 64 * 1.07 / 0.85;
+    if (c64 < c2 && force_cta != 2) {
+      pl.cta = 1;
+      pl.tn = 64;
+    }
+  }
+  if (const int f = g_force_tn.load(std::memory_order_relaxed))
+    pl.tn = (f == 192 && pl.cta == 2 && !emu) ? 192 : (f == 64 && pl.cta == 1 ? 64 : 128);
+  else if (pl.tn == 64 && pl.cta == 2)
+    pl.tn = 128;
   pl.tiles_m = (int)((m + oz::kPM * pl.cta - 1) / (oz::kPM * pl.cta));
   pl.tiles_n = (int)((n + pl.tn - 1) / pl.tn);
   pl.pairs = 0;
@@ -408,11 +428,18 @@ int oz_split_pad(void* coeff, int64_t ld_coeff, int64_t rows, int type2, int s, 
 }
 
 int oz_set_pair_variant(int cta_group, int tile_n, int raster_group) {
-  if (cta_group < 0 || cta_group > 2 || (tile_n != 0 && tile_n != 128 && tile_n != 192) || raster_group < 0)
+  if (cta_group < 0 || cta_group > 2 || (tile_n != 0 && tile_n != 64 && tile_n != 128 && tile_n != 192) ||
+      raster_group < 0)
     return OZ_EINVAL;
   g_force_cta.store(cta_group, std::memory_order_relaxed);
   g_force_tn.store(tile_n, std::memory_order_relaxed);
   g_force_group.store(raster_group, std::memory_order_relaxed);
+  return OZ_OK;
+}
+
+int oz_set_epilogue_warps(int warps) {
+  if (warps != 8 && warps != 12) return OZ_EINVAL;
+  g_epi_warps.store(warps, std::memory_order_relaxed);
   return OZ_OK;
 }
 
@@ -597,10 +624,13 @@ static int pair_gemm_impl(const void* a_planes, const void* b_planes, int64_t ld
     cudaStreamWaitEvent(cst, ev, 0);
     cudaEventDestroy(ev);
   }
-  if (cta == 1)
+  if (cta == 1 && tn == 64)
+    rc = emu ? launch_pair_fmt<true, 1, 64>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 1, 64>(ma, mb, P, tiles, st);
+  else if (cta == 1)
     rc = emu ? launch_pair_fmt<true, 1, 128>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 1, 128>(ma, mb, P, tiles, st);
-  else if (tn == 192)
-    rc = launch_pair_fmt<false, 2, 192>(ma, mb, P, tiles, st);  // hardware mode only (plan_pair)
+  else if (tn == 192)  // hardware mode only (plan_pair)
+    rc = g_epi_warps.load(std::memory_order_relaxed) == 12 ? launch_pair_fmt<false, 2, 192, 12>(ma, mb, P, tiles, st)
+                                                           : launch_pair_fmt<false, 2, 192, 8>(ma, mb, P, tiles, st);
   else
     rc = emu ? launch_pair_fmt<true, 2, 128>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 2, 128>(ma, mb, P, tiles, st);
   if (rc) return rc;

@@ -44,8 +44,9 @@
 namespace oz {
 
 constexpr int kPM = 128;                   // per-CTA output rows
-constexpr int kEpiWarps = 8;
-constexpr int kPThreads = 128 + 32 * kEpiWarps;
+constexpr int kEpiWarps = 8;                // default epilogue warps (two threads per C row)
+constexpr int kLeadWarps = 4;               // warpgroup 0 (setmaxnreg is warpgroup-wide): warp 0 TMA, warp 1 MMA
+constexpr int kPThreads = 32 * kLeadWarps + 32 * kEpiWarps;
 constexpr int kTmemCols = 512;             // whole TMEM: accumulators (+ part of Cb for N > 128)
 constexpr int kPaceBlocks = 64;            // k-blocks per cross-CTA pacing step (8192 FP8 / 4096 FP16 K)
 
@@ -58,18 +59,30 @@ constexpr int kPaceBlocks = 64;            // k-blocks per cross-CTA pacing step
 // columns of FP64), so the ~60-op integer add is instantiated once in a rolled
 // chunk loop — fully unrolled over 64 register columns it overflowed the
 // instruction cache (ncu: "no instruction" was the top stall).
-template <int kCta, int kN, bool kEmu>
+//   kEpi = 12 (N = 192, hardware mode): three epilogue threads per C row, each
+//   with 48 Cb columns in registers and 16 in TMEM (one chunk), so the work
+//   left for the per-pair FP64 gap is a third smaller and its dependent TMEM
+//   load/store chain one chunk long (512 threads: 128 registers each).
+template <int kCta, int kN, bool kEmu, int kEpi = kEpiWarps>
 struct PairCfg {
+  static constexpr int kThreads = 32 * kLeadWarps + 32 * kEpi;
+  static constexpr int kParts = kEpi / 4;                     // epilogue threads per C row
   static constexpr int kBRows = kN / kCta;                    // B rows staged per CTA
   static constexpr int kStageBytes = (kPM + kBRows) * 128;    // per CTA
-  static constexpr int kRegCols = kEmu ? 0 : 128;             // C columns whose Cb lives in registers
-  static constexpr int kAccBufs = (kEmu || kN != 128) ? 2 : 4;
+  static constexpr int kRegCols = kEmu ? 0 : (kEpi == 12 ? kN * 3 / 4 : (kN < 128 ? kN : 128));  // Cb cols in registers
+  static constexpr int kRegHalf = kRegCols / kParts;          // ... per epilogue thread
+  static constexpr int kAccBufs = kN == 64 ? 4 : ((kEmu || kN != 128) ? 2 : 4);
   static constexpr int kTmCols = kN - kRegCols;               // C columns whose Cb lives in TMEM
   static constexpr int kCbTmem = kAccBufs * kN;               // first TMEM column of that Cb
   static constexpr int kSmemBudget = 227 * 1024 - 2048;
   static constexpr int kStages = kSmemBudget / kStageBytes > 10 ? 10 : kSmemBudget / kStageBytes;
   static_assert(kCbTmem + 2 * kTmCols <= kTmemCols, "TMEM budget");
-  static_assert(kN == 128 || kCta == 2, "N > 128 needs the CTA pair");
+  static_assert(kN <= 128 || kCta == 2, "N > 128 needs the CTA pair");
+  static_assert(kRegHalf % 16 == 0 && (kN - kRegCols) % (16 * kParts) == 0, "16-column TMEM chunks per thread");
+  static_assert(kEpi == 8 || (kEpi == 12 && !kEmu), "12 epilogue warps: hardware FP64 mode only");
+  static constexpr int kRegLo = 40;                           // setmaxnreg: producer / MMA warps
+  static constexpr int kRegHi = kEpi == 8 ? 232 : 152;        // setmaxnreg: epilogue warps
+  static_assert(kLeadWarps * kRegLo + kEpi * kRegHi <= 2048, "register file");
 };
 
 template <int kCta, int kN, bool kEmu>
@@ -524,11 +537,11 @@ __global__ void prep_eb_kernel(const int32_t* __restrict__ expo_b, int n, int kn
   }
 }
 
-template <bool kEmu, int kCta, int kElemBytes, int kN>
-__global__ void __launch_bounds__(kPThreads, 1)
+template <bool kEmu, int kCta, int kElemBytes, int kN, int kEpi = kEpiWarps>
+__global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
     pair_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const PairParams P) {
-  using Cfg = PairCfg<kCta, kN, kEmu>;
+  using Cfg = PairCfg<kCta, kN, kEmu, kEpi>;
   constexpr int kStages = Cfg::kStages;
   constexpr int kAccBufs = Cfg::kAccBufs;
   extern __shared__ uint8_t smem_raw[];
@@ -564,7 +577,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
     for (int i = 0; i < kAccBufs; ++i) {
       mbar_init(&s.acc_full[i], 1);
-      mbar_init(&s.acc_empty[i], kEpiWarps * kCta);
+      mbar_init(&s.acc_empty[i], kEpi * kCta);
     }
     fence_barrier_init();
   }
@@ -574,8 +587,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
   tc_fence_after();
   const uint32_t tmem = s.tmem_base;
 
-  if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+  if (warp < kLeadWarps) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::kRegLo));
     if (warp == 0) {
       // ───────── TMA producer (both CTAs of a pair load their own halves) ─────────
       if (elect_one()) {
@@ -685,12 +698,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Cfg::kRegHi));
     // ───────── epilogue: ordered FP64 accumulation ─────────
     constexpr int kRegCols = Cfg::kRegCols;
-    constexpr int kTmHalf = Cfg::kTmCols / 2;  // TMEM-resident Cb columns per thread
+    constexpr int kTmHalf = Cfg::kTmCols / Cfg::kParts;  // TMEM-resident Cb columns per thread
     const int quad = warp & 3;               // TMEM lane quadrant this warp may access
-    const int half = (warp - 4) >> 2;        // register Cb: cols [64h, 64h+64); TMEM Cb: [kRegCols + kTmHalf*h, +kTmHalf)
+    constexpr int kRegHalf = Cfg::kRegHalf;
+    const int half = (warp - kLeadWarps) >> 2;        // part: register Cb cols [kRegHalf h, +kRegHalf); TMEM Cb: [kRegCols + kTmHalf*h, +kTmHalf)
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
     const uint32_t cb_tmem = tmem + lane_base + Cfg::kCbTmem + half * 2 * kTmHalf;  // 2 words per FP64
     uint32_t flags = 0;
@@ -706,9 +720,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
       // Cb is kept as raw FP64 bit patterns; in emulated mode no double-typed
       // value may exist at all, or nvcc turns bit tricks into FP64 instructions.
       using Acc = uint64_t;
-      Acc cb[kRegCols > 0 ? 64 : 1];
+      Acc cb[kRegCols > 0 ? kRegHalf : 1];
 #pragma unroll
-      for (int j = 0; j < (kRegCols > 0 ? 64 : 1); ++j) cb[j] = Acc(0);
+      for (int j = 0; j < (kRegCols > 0 ? kRegHalf : 1); ++j) cb[j] = Acc(0);
       if constexpr (kTmHalf > 0) {
         uint32_t z[32];
 #pragma unroll
@@ -754,8 +768,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
           // Pull this pair's B-exponent lines into L1 now: the loads that use them
           // come after the first DADD, i.e. in the short window in which the
           // epilogue's DADDs can drain, where an L2 miss would stall.
-          if (lane < (kRegCols > 0 ? 2 : 0) + (kTmHalf * 4 + 127) / 128) {
-            const int32_t* pf = lane < (kRegCols > 0 ? 2 : 0) ? ebq + half * 64 + lane * 32
+          constexpr int kRegLines = (kRegHalf + 31) / 32;  // 128-byte lines of this thread's register-part exponents
+          if (lane < kRegLines + (kTmHalf * 4 + 127) / 128) {
+            const int32_t* pf = lane < kRegLines ? ebq + half * kRegHalf + lane * 32
                                                                : ebq + kRegCols + half * kTmHalf;
             asm volatile("prefetch.global.L1 [%0];" ::"l"(pf));
           }
@@ -764,13 +779,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
           // accumulated (the wait names the registers so no use is hoisted above it).
           if constexpr (kRegCols > 0) {
             uint32_t g[2][16];
-            tmem_ld16(gaddr + half * 64, g[0]);
+            tmem_ld16(gaddr + half * kRegHalf, g[0]);
             tmem_ld_wait_regs(g[0]);
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-              if (ch + 1 < 4) tmem_ld16(gaddr + half * 64 + (ch + 1) * 16, g[(ch + 1) & 1]);
-              accumulate16<kEmu>(g[ch & 1], ebq + half * 64 + ch * 16, ea_sh, safe, cb + ch * 16, flags);
-              if (ch + 1 < 4) tmem_ld_wait_regs(g[(ch + 1) & 1]);
+            for (int ch = 0; ch < kRegHalf / 16; ++ch) {
+              if (ch + 1 < kRegHalf / 16) tmem_ld16(gaddr + half * kRegHalf + (ch + 1) * 16, g[(ch + 1) & 1]);
+              accumulate16<kEmu>(g[ch & 1], ebq + half * kRegHalf + ch * 16, ea_sh, safe, cb + ch * 16, flags);
+              if (ch + 1 < kRegHalf / 16) tmem_ld_wait_regs(g[(ch + 1) & 1]);
             }
           }
           if (tr) P.trace[acc_it * 8 + 7] = clock64();
@@ -812,7 +827,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       // are warp-collective (.sync.aligned): issue them outside the row guard.
       const bool store = !(OZ_DIAGNOSTICS && (P.debug & 8));  // diagnostics: bit 3 skips the C stores
       if constexpr (kRegCols > 0)
-        if (row < P.m && store) store_row<kEmu>(P, row, tn * kN + half * 64, cb, 64, flags);
+        if (row < P.m && store) store_row<kEmu>(P, row, tn * kN + half * kRegHalf, cb, kRegHalf, flags);
       if constexpr (kTmHalf > 0) {
 #pragma unroll(kEmu ? 1 : kTmHalf / 16)
         for (int ch = 0; ch < kTmHalf / 16; ++ch) {
@@ -831,8 +846,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
       // on the band counter (cuStreamWaitValue32) can move finished bands to the
       // host while later tiles compute.
       if (P.band_done) {
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-        if (threadIdx.x == 128) {
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpi) : "memory");
+        if (threadIdx.x == 32 * kLeadWarps) {
           __threadfence_system();
           atomicAdd(P.band_done + tm / P.group, 1u);
         }
@@ -847,7 +862,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
 }
 
 template <int kCta, int kN, bool kEmu>
-size_t pair_gemm_smem_bytes() {
+size_t pair_gemm_smem_bytes() {  // independent of the epilogue warp count
   return sizeof(PairSmem<kCta, kN, kEmu>) + 1024;
 }
 

@@ -70,7 +70,8 @@ CASES = [
 @pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}x{c[1]}x{c[2]}-{c[4]}-{c[5]}-kb{c[6]}-emu{int(c[7])}"
                                              f"-ms{c[8]}-{c[9][:5]}-cut{c[10]}" for c in CASES])
 @pytest.mark.parametrize("skip", [True, False])
-@pytest.mark.parametrize("variant", [("1", "128"), ("2", "128"), ("2", "192")], ids=lambda v: f"cta{v[0]}-n{v[1]}")
+@pytest.mark.parametrize("variant", [("1", "64"), ("1", "128"), ("2", "128"), ("2", "192")],
+                         ids=lambda v: f"cta{v[0]}-n{v[1]}")
 def test_oz_gemm_bitwise(cuda, case, skip, variant, pair_variant):
     import oracle
 
@@ -275,7 +276,8 @@ FIXED_CASES = [
 
 @pytest.mark.parametrize("case", FIXED_CASES, ids=[f"{c[0]}x{c[1]}x{c[2]}-{c[4]}-kb{c[5]}-emu{int(c[6])}"
                                                    f"-ms{c[7]}-{c[8][:5]}-cut{c[9]}" for c in FIXED_CASES])
-@pytest.mark.parametrize("variant", [("1", "128"), ("2", "128"), ("2", "192")], ids=lambda v: f"cta{v[0]}-n{v[1]}")
+@pytest.mark.parametrize("variant", [("1", "64"), ("1", "128"), ("2", "128"), ("2", "192")],
+                         ids=lambda v: f"cta{v[0]}-n{v[1]}")
 def test_fixed_step_grouped_bitwise(cuda, case, variant, pair_variant):
     """slice_exponents="fixed" (opt-in): fixed-step slices and level-grouped
     tensor-core accumulation, bitwise against the CPU restatement
@@ -440,3 +442,26 @@ def test_graph_replay_bitwise(cuda, kw):
     A[5, 7] = float("nan")
     with pytest.raises(ValueError):
         oz.oz_gemm_device(A, B, cfg, out=Cg, graph=True)
+
+
+@pytest.mark.parametrize("kw", [{}, {"fp64_emulation": True}, {"pair_cutoff": 9, "slice_exponents": "fixed"},
+                                {"k_block": 512}], ids=["defaults", "emu", "fixed9", "kb512"])
+def test_variants_agree_multiwave(cuda, kw, pair_variant):
+    """Every kernel variant (1-CTA 128x64 and 128x128, CTA-pair 256x128 and
+    256x192) over several persistent-tile waves gives bitwise the same C."""
+    torch = cuda
+    oz = _oz()
+    rng = np.random.default_rng(21)
+    A = torch.from_numpy(spread_matrix(rng, 2048, 1024, 1.0)).cuda()
+    B = torch.from_numpy(spread_matrix(rng, 1024, 1920, 1.0)).cuda()
+    cfg = oz.GemmConfig(oz.get_format("fp8e4m3"), oz.get_format("fp32"), **kw)
+    ref = None
+    for cta, tn in ((2, 192), (1, 64), (1, 128), (2, 128)):
+        if kw.get("fp64_emulation") and tn == 192:
+            continue
+        pair_variant(cta, tn)
+        C, _ = oz.oz_gemm_device(A, B, cfg)
+        if ref is None:
+            ref = C.clone()
+        else:
+            assert torch.equal(C.view(torch.int64), ref.view(torch.int64)), (cta, tn)
