@@ -86,25 +86,28 @@ FP64_OPS = re.compile(r"\b(DFMA|DADD|DMUL|DSETP|DMNMX|DSET|F2F\.F64|F2F\.F32\.F6
 # pair_gemm_kernel<emu=true, ...>, and the mode-independent helpers (code table,
 # zero padding, transpose, B-exponent prep, tile counts).
 EMU_SPLIT = re.compile(r"split_fused_kernelILi\d+ELi\d+ELi\d+ELi\d+ELb1EE")
+EMU_COLS = re.compile(r"col_slice_kernelILi\d+ELb1EE")  # fixed-step in-place column split, emulated
 EMU_HELPERS = ("build_code_table_kernel", "pad_planes_kernel", "transpose_kernel", "prep_eb_kernel",
-               "tile_counts_kernel")
+               "tile_counts_kernel", "col_stats_kernel", "col_finish_kernel")
 
 
 def is_emulated_path_kernel(name: str) -> bool:
     return ("pair_gemm_kernelILb1E" in name or EMU_SPLIT.search(name) is not None
-            or any(h in name for h in EMU_HELPERS))
+            or EMU_COLS.search(name) is not None or any(h in name for h in EMU_HELPERS))
 
 
 def test_emulated_kernels_have_no_fp64_arithmetic(lib):
     """north_star: the emulated path contains no DFMA/DADD/DMUL (or any other
-    FP64 instruction) in its SASS — checked over all 20 emulated split / pair-GEMM
-    instantiations and the 5 helpers they run with."""
+    FP64 instruction) in its SASS — checked over all 24 emulated split / pair-GEMM
+    instantiations (16 row splits, 2 in-place column splits, 6 pair GEMMs) and
+    the 7 helpers they run with."""
     from paper_2508_00441_b200 import _lib
 
     sel = _sass_of(_lib.LIB_PATH, is_emulated_path_kernel)
     n_split = sum(1 for k in sel if EMU_SPLIT.search(k))
+    n_cols = sum(1 for k in sel if EMU_COLS.search(k))
     n_pair = sum(1 for k in sel if "pair_gemm_kernelILb1E" in k)
-    assert n_split == 16 and n_pair == 4, (n_split, n_pair)
+    assert n_split == 16 and n_cols == 2 and n_pair == 6, (n_split, n_cols, n_pair)
     assert all(any(h in k for k in sel) for h in EMU_HELPERS)
     for name, lines in sel.items():
         bad = [ln for ln in lines if FP64_OPS.search(ln)]

@@ -33,7 +33,10 @@ def main(path):
         for k, m in KEYS.items():
             if m in hdr:
                 i = hdr.index(m)
-                v = float(vals[i].replace(",", ""))
+                try:
+                    v = float(vals[i].replace(",", ""))
+                except ValueError:  # "no data" (e.g. no tensor pipe in a split kernel)
+                    continue
                 d[k] = v * SCALE.get(units[i], 1) if "pct" not in k else v
         if "dram_read_bytes" in d:
             d["traffic_bytes_per_launch"] = d["dram_read_bytes"] + d.get("dram_write_bytes", 0)
