@@ -205,7 +205,8 @@ int oz_dd_gemm(const double* A, const double* B, double* C, int64_t m, int64_t n
 
 /* out[i] = a[i] + b[i] on FP64 bit patterns with the integer-only emulation:
  * mode 0 = emu_add (restates fp64emu._add_core, fp64emu.py:193-251; range errors
- * set OZ_FLAG_EMU_RANGE), mode 1 = the epilogue's fast_add (same results).
+ * set OZ_FLAG_EMU_RANGE), mode 1 = the epilogue's fast_add, mode 2 = the
+ * emulated epilogue's add_lean (same results).
  * Backs the CLI's `verify --suite fp64emu` (cli.py:190-222). */
 int oz_emu_add_batch(const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t n, int mode, uint32_t* flags,
                      void* stream);

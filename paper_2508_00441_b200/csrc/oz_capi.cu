@@ -302,8 +302,17 @@ PairPlan plan_pair(int64_t m, int64_t n, int64_t kb, int elem_bytes, int sx, int
 __global__ void emu_add_batch_kernel(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
                                      uint64_t* __restrict__ out, int64_t n, int mode, uint32_t* flags) {
   uint32_t f = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (mode == 2) {  // add_lean on its domain (normal or zero operands), emu_add otherwise / when slow
+      const uint32_t ea = (uint32_t)(a[i] >> 52) & 0x7FFu, eb = (uint32_t)(b[i] >> 52) & 0x7FFu;
+      const bool dom = (ea != 0 || (a[i] << 1) == 0) && (eb != 0 || (b[i] << 1) == 0) && ea != 0x7FFu && eb != 0x7FFu;
+      bool slow = true;
+      const uint64_t r = dom ? oz::add_lean(a[i], b[i], slow) : 0ull;
+      out[i] = slow ? oz::emu_add(a[i], b[i], f) : r;
+      continue;
+    }
     out[i] = mode == 0 ? oz::emu_add(a[i], b[i], f) : oz::fast_add<true>(a[i], b[i], f);
+  }
   if (f) atomicOr(flags, f);
 }
 
@@ -675,7 +684,7 @@ int oz_pair_gemm_grouped(const void* a_planes, const void* b_planes, int64_t ld_
 
 int oz_emu_add_batch(const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t n, int mode, uint32_t* flags,
                      void* stream) {
-  if (n < 0 || (mode != 0 && mode != 1)) return OZ_EINVAL;
+  if (n < 0 || mode < 0 || mode > 2) return OZ_EINVAL;
   if (n == 0) return OZ_OK;
   if (!a || !b || !out || !flags) return OZ_EINVAL;
   const int64_t blocks = (n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096;

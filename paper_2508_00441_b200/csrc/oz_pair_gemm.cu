@@ -405,10 +405,13 @@ OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_sh, int e
       uint32_t slow = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
+        // Cb is +0 or normal and every term normal or zero: add_lean's domain
+        // (a zero term returns Cb unchanged); a result that may leave the normal
+        // range goes to the checked emu_add below.
         bool sl;
-        const uint64_t r = add_nb(cb[8 * h + j], t[j], sl);
-        slow |= (uint32_t)(sl && t[j] != 0) << j;  // a zero term leaves Cb as is
-        cb[8 * h + j] = (sl || t[j] == 0) ? cb[8 * h + j] : r;
+        const uint64_t r = add_lean(cb[8 * h + j], t[j], sl);
+        slow |= (uint32_t)sl << j;
+        cb[8 * h + j] = sl ? cb[8 * h + j] : r;
       }
       if (slow) {
 #pragma unroll
