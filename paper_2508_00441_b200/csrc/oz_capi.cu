@@ -307,7 +307,7 @@ __global__ void emu_add_batch_kernel(const uint64_t* __restrict__ a, const uint6
       const uint32_t ea = (uint32_t)(a[i] >> 52) & 0x7FFu, eb = (uint32_t)(b[i] >> 52) & 0x7FFu;
       const bool dom = (ea != 0 || (a[i] << 1) == 0) && (eb != 0 || (b[i] << 1) == 0) && ea != 0x7FFu && eb != 0x7FFu;
       bool slow = true;
-      const uint64_t r = dom ? oz::add_lean(a[i], b[i], slow) : 0ull;
+      const uint64_t r = dom ? oz::add_lean<false>(a[i], b[i], slow) : 0ull;
       out[i] = slow ? oz::emu_add(a[i], b[i], f) : r;
       continue;
     }

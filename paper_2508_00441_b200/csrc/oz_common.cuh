@@ -310,6 +310,9 @@ OZ_DEVICE uint64_t add_nb(uint64_t a, uint64_t b, bool& slow) {
 // 62..10 (10 guard bits), the smaller aligned with a sticky bit, the sum
 // normalised to bit 63 by one left shift (a carry leaves it at 63: shift 0),
 // RNE on the 11 bits below the 53-bit significand.
+// kSubIn: also send subnormal operands to the slow path (hardware-mode callers,
+// where an earlier DADD may have left Cb subnormal).
+template <bool kSubIn = false>
 OZ_DEVICE uint64_t add_lean(uint64_t a, uint64_t b, bool& slow) {
   const uint32_t ah = (uint32_t)(a >> 32), al = (uint32_t)a, bh = (uint32_t)(b >> 32), bl = (uint32_t)b;
   const uint32_t amh = ah & 0x7FFFFFFFu, bmh = bh & 0x7FFFFFFFu;
@@ -344,6 +347,7 @@ OZ_DEVICE uint64_t add_lean(uint64_t a, uint64_t b, bool& slow) {
   const uint32_t up = (rem + ((uint32_t)sig & 1u) + 1023u) >> 11;
   const uint64_t r = ((uint64_t)sgn << 32) | ((((uint64_t)(uint32_t)(e - 1)) << 52) + sig + up);
   slow = (unsigned)(e - 1) >= 2045u && m != 0;
+  if constexpr (kSubIn) slow |= (ex == 0 && (xh | xl) != 0u) || (ey == 0 && (yh | yl) != 0u);
   return m == 0 ? 0ull : r;
 }
 

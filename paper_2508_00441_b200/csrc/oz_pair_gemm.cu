@@ -33,6 +33,9 @@
 #ifndef OZ_TERM_FMA
 #define OZ_TERM_FMA 1  // HW-mode safe terms: DFMA(double(G), 2^(eA+eB), Cb) instead of bit assembly + DADD
 #endif
+#ifndef OZ_HW_INT_TMEM
+#define OZ_HW_INT_TMEM 0  // 1: hardware mode adds the TMEM third of Cb with integer add_lean, first (A/B: slower)
+#endif
 #ifndef OZ_DIAGNOSTICS
 #define OZ_DIAGNOSTICS 0  // 1: per-pair clock trace + OZ_DEBUG_MODE hooks (tools/ only; never the product)
 #endif
@@ -373,12 +376,14 @@ OZ_DEVICE void tmem_ld_wait_regs(uint32_t (&r)[16]) {
 //   in the FP64 field, + (eA + eB + 896) << 20 rebiases it, the sign is or-ed
 //   back, the low word is G << 29).  Otherwise the checked make_term handles
 //   range errors.
-//   Emulated mode: integer fast_add (emu_add for the rare operands it cannot take).
-template <bool kEmu>
+//   kInt (always in emulated mode; the TMEM-resident part of Cb in hardware
+//   mode): integer add_lean (bit-identical RNE), the rare operands it cannot take
+//   going to emu_add (emulated) or DADD (hardware).
+template <bool kEmu, bool kInt = kEmu>
 OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_sh, int ea_sh, bool safe, uint64_t* cb,
                             uint32_t& flags) {
   const int4* ebv = reinterpret_cast<const int4*>(eb_sh);
-  if constexpr (kEmu) {
+  if constexpr (kInt) {
     // Emulated mode: groups of 8 terms added with the branch-free integer core
     // (independent chains the scheduler can interleave); the rare operands it
     // cannot take (zero/subnormal/Inf, possible under/overflow) go through
@@ -398,7 +403,7 @@ OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_sh, int e
             const uint32_t hi = (((gv >> 3) & 0x0FFFFFFFu) + (uint32_t)(ea_sh + e[u])) | (gv & 0x80000000u);
             t[4 * v + u] = ((gv << 1) != 0u) ? (((uint64_t)hi << 32) | (uint64_t)(gv << 29)) : 0ull;
           } else {
-            t[4 * v + u] = make_term<true>(gv, (ea_sh >> 20) + (e[u] >> 20), bad);
+            t[4 * v + u] = make_term<kEmu>(gv, (ea_sh >> 20) + (e[u] >> 20), bad);
           }
         }
       }
@@ -409,14 +414,14 @@ OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_sh, int e
         // (a zero term returns Cb unchanged); a result that may leave the normal
         // range goes to the checked emu_add below.
         bool sl;
-        const uint64_t r = add_lean(cb[8 * h + j], t[j], sl);
+        const uint64_t r = add_lean<!kEmu>(cb[8 * h + j], t[j], sl);
         slow |= (uint32_t)sl << j;
         cb[8 * h + j] = sl ? cb[8 * h + j] : r;
       }
       if (slow) {
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if ((slow >> j) & 1u) cb[8 * h + j] = slow_add<true>(cb[8 * h + j], t[j], &flags);
+          if ((slow >> j) & 1u) cb[8 * h + j] = slow_add<kEmu>(cb[8 * h + j], t[j], &flags);
       }
     }
     if (bad) flags |= FLAG_TERM_RANGE;
@@ -705,6 +710,10 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
     // ───────── epilogue: ordered FP64 accumulation ─────────
     constexpr int kRegCols = Cfg::kRegCols;
     constexpr int kTmHalf = Cfg::kTmCols / Cfg::kParts;  // TMEM-resident Cb columns per thread
+    // TMEM-resident Cb with integer adds (always in emulated mode; hardware mode:
+    // OZ_HW_INT_TMEM), processed before the register part.
+    constexpr bool kTmInt = kEmu || OZ_HW_INT_TMEM;
+    constexpr bool kTmFirst = !kEmu && OZ_HW_INT_TMEM;
     const int quad = warp & 3;               // TMEM lane quadrant this warp may access
     constexpr int kRegHalf = Cfg::kRegHalf;
     const int half = (warp - kLeadWarps) >> 2;        // part: register Cb cols [kRegHalf h, +kRegHalf); TMEM Cb: [kRegCols + kTmHalf*h, +kTmHalf)
@@ -778,6 +787,35 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
             asm volatile("prefetch.global.L1 [%0];" ::"l"(pf));
           }
           const uint32_t gaddr = tmem + lane_base + buf * kN;
+          auto tmem_part = [&]() {
+            // Integer adds (kTmInt): rolled, so the code stays in the instruction cache.
+#pragma unroll(kTmInt || kTmHalf < 16 ? 1 : kTmHalf / 16)
+            for (int ch = 0; ch < kTmHalf / 16; ++ch) {
+              uint32_t g[16], w[32];
+              tmem_ld16(gaddr + kRegCols + half * kTmHalf + ch * 16, g);
+              tmem_ld32(cb_tmem + ch * 32, w);
+              tmem_ld_wait();
+              Acc c16[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const uint64_t b = (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
+                c16[j] = b;
+              }
+              accumulate16<kEmu, kTmInt>(g, ebq + kRegCols + half * kTmHalf + ch * 16, ea_sh, safe, c16, flags);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const uint64_t b = c16[j];
+                w[2 * j] = (uint32_t)b;
+                w[2 * j + 1] = (uint32_t)(b >> 32);
+              }
+              tmem_st32(cb_tmem + ch * 32, w);
+            }
+            tmem_st_wait();
+          };
+          // Hardware mode, integer TMEM part: issued first, while the tensor pipe runs
+          // (integer ops are not held back by the MMAs; the register part's DFMAs are).
+          if constexpr (kTmHalf > 0 && kTmFirst) tmem_part();
+
           // Software-pipelined TMEM reads: chunk ch+1 loads while chunk ch is
           // accumulated (the wait names the registers so no use is hoisted above it).
           if constexpr (kRegCols > 0) {
@@ -792,30 +830,7 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
             }
           }
           if (tr) P.trace[acc_it * 8 + 7] = clock64();
-          if constexpr (kTmHalf > 0) {
-#pragma unroll(kEmu ? 1 : kTmHalf / 16)
-            for (int ch = 0; ch < kTmHalf / 16; ++ch) {
-              uint32_t g[16], w[32];
-              tmem_ld16(gaddr + kRegCols + half * kTmHalf + ch * 16, g);
-              tmem_ld32(cb_tmem + ch * 32, w);
-              tmem_ld_wait();
-              Acc c16[16];
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                const uint64_t b = (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
-                c16[j] = b;
-              }
-              accumulate16<kEmu>(g, ebq + kRegCols + half * kTmHalf + ch * 16, ea_sh, safe, c16, flags);
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                const uint64_t b = c16[j];
-                w[2 * j] = (uint32_t)b;
-                w[2 * j + 1] = (uint32_t)(b >> 32);
-              }
-              tmem_st32(cb_tmem + ch * 32, w);
-            }
-            tmem_st_wait();
-          }
+          if constexpr (kTmHalf > 0 && !kTmFirst) tmem_part();
         }
         tc_fence_before();
         __syncwarp();
