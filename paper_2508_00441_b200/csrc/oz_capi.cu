@@ -243,6 +243,8 @@ struct PairPlan {
 std::atomic<int> g_force_cta{0}, g_force_tn{0}, g_force_group{0};
 // Epilogue warps of the CTA-pair N = 192 hardware-mode kernel (8 or 12).
 std::atomic<int> g_epi_warps{8};
+// Pair-GEMM schedule: 0 overlapped epilogue, 1 exclusive epilogue windows.
+std::atomic<int> g_pair_sched{0};
 
 PairPlan plan_pair(int64_t m, int64_t n, int64_t kb, int elem_bytes, int sx, int sy, int pair_cutoff, int emu) {
   PairPlan pl{};
@@ -251,37 +253,40 @@ PairPlan plan_pair(int64_t m, int64_t n, int64_t kb, int elem_bytes, int sx, int
   // emulated mode (ALU-bound epilogue: 4 accumulators absorb its jitter, and all
   // of Cb sits in registers; measured 144 -> 109 ms at n = 8192, pair_cutoff = 11).
   // oz_set_pair_variant(cta_group, tile_n, group) overrides (experiments, tests).
-  pl.cta = m > oz::kPM ? 2 : 1;
+  // Variant by a wave-cost model: time ~ waves x columns per CTA / efficiency,
+  // efficiencies per output column measured at n = 8192 (profiles/variant_sweep_r01.txt,
+  // profiles/variant_kb_r02.txt): 256 x 192 CTA pair 1.00; 256 x 128 pair 0.92, 128 x 128
+  // single CTA 0.935, except short FP8 pairs (kb <= 2048: the 4-accumulator 1-CTA kernel
+  // absorbs the epilogue better, 1.10); 128 x 64 single CTA 0.795.  N = 192 exists in
+  // hardware mode only; a single 128-row slab uses single-CTA tiles.
   const int force_cta = g_force_cta.load(std::memory_order_relaxed);
-  if (force_cta) pl.cta = force_cta == 1 ? 1 : 2;
-  pl.tn = 128;
-  if (pl.cta == 2 && n > 128 && !emu) {
-    // N = 192 unless tile quantisation favours N = 128: time ~ waves x N / efficiency,
-    // with N = 192 measured ~1.07x more efficient per column (n = 2048: N = 128 is
-    // 36% faster, n = 4096 even, n >= 6144 N = 192 wins; profiles/variant_sweep_r01.txt).
-    const int64_t units = num_sms() / 2, tm = (m + 2 * oz::kPM - 1) / (2 * oz::kPM);
-    const int64_t w192 = (tm * ((n + 191) / 192) + units - 1) / units;
-    const int64_t w128 = (tm * ((n + 127) / 128) + units - 1) / units;
-    pl.tn = (double)w192 * 192.0 <= (double)w128 * 128.0 * 1.07 ? 192 : 128;
-  }
+  const int force_tn = g_force_tn.load(std::memory_order_relaxed);
   {
-    // Small problems: 128 x 64 single-CTA tiles (every SM busy, half the
-    // epilogue work per CTA and pair) when the CTA-pair tiles leave SMs idle.
-    // Cost ~ waves x per-CTA columns / relative efficiency (N = 64: ~0.85 of N = 128).
-    const int64_t sms = num_sms(), units = sms / pl.cta, rows = (int64_t)oz::kPM * pl.cta;
-    const int64_t t2 = ((m + rows - 1) / rows) * ((n + pl.tn - 1) / pl.tn);
-    const double c2 = (double)((t2 + units - 1) / units) * pl.tn * (pl.tn == 192 ? 1.0 : 1.07);
-    const int64_t t64 = ((m + oz::kPM - 1) / oz::kPM) * ((n + 63) / 64);
-    const double c64 = (double)((t64 + sms - 1) / sms) * 64 * 1.07 / 0.85;
-    if (c64 < c2 && force_cta != 2) {
-      pl.cta = 1;
-      pl.tn = 64;
+    const int64_t sms = num_sms();
+    const bool short_fp8 = elem_bytes == 1 && kb <= 2048 && !emu;
+    struct Cand { int cta, tn; double eff; };
+    const Cand cands[4] = {{2, 192, 1.0}, {2, 128, 0.92}, {1, 128, short_fp8 ? 1.10 : 0.935}, {1, 64, 0.795}};
+    double best = 0.0;
+    pl.cta = 0;
+    for (const Cand& c : cands) {
+      if (c.tn == 192 && emu) continue;
+      if (c.cta == 2 && m <= oz::kPM) continue;
+      if (force_cta && c.cta != (force_cta == 1 ? 1 : 2)) continue;
+      if (force_tn && c.tn != force_tn) continue;
+      const int64_t units = sms / c.cta, rows = (int64_t)oz::kPM * c.cta;
+      const int64_t tiles = ((m + rows - 1) / rows) * ((n + c.tn - 1) / c.tn);
+      const double cost = (double)((tiles + units - 1) / units) * c.tn / c.eff;
+      if (pl.cta == 0 || cost < best) {
+        best = cost;
+        pl.cta = c.cta;
+        pl.tn = c.tn;
+      }
+    }
+    if (pl.cta == 0) {  // forced combination that does not exist (e.g. N = 192 emulated): nearest valid
+      pl.cta = force_cta == 1 || m <= oz::kPM ? 1 : 2;
+      pl.tn = (force_tn == 64 && pl.cta == 1) ? 64 : 128;
     }
   }
-  if (const int f = g_force_tn.load(std::memory_order_relaxed))
-    pl.tn = (f == 192 && pl.cta == 2 && !emu) ? 192 : (f == 64 && pl.cta == 1 ? 64 : 128);
-  else if (pl.tn == 64 && pl.cta == 2)
-    pl.tn = 128;
   pl.tiles_m = (int)((m + oz::kPM * pl.cta - 1) / (oz::kPM * pl.cta));
   pl.tiles_n = (int)((n + pl.tn - 1) / pl.tn);
   pl.pairs = 0;
@@ -446,6 +451,12 @@ int oz_set_pair_variant(int cta_group, int tile_n, int raster_group) {
   return OZ_OK;
 }
 
+int oz_set_pair_schedule(int mode) {
+  if (mode != 0 && mode != 1) return OZ_EINVAL;
+  g_pair_sched.store(mode, std::memory_order_relaxed);
+  return OZ_OK;
+}
+
 int oz_set_epilogue_warps(int warps) {
   if (warps != 8 && warps != 12) return OZ_EINVAL;
   g_epi_warps.store(warps, std::memory_order_relaxed);
@@ -566,6 +577,7 @@ static int pair_gemm_impl(const void* a_planes, const void* b_planes, int64_t ld
     P.g_hi = 127 + lg;
   }
   P.trace = nullptr; P.trace_cap = 0; P.debug = 0;
+  P.serial = g_pair_sched.load(std::memory_order_relaxed);
 #if OZ_DIAGNOSTICS
   // Diagnostic builds only (tools/): OZ_DEBUG_MODE bits, L2 hints, and
   // OZ_TRACE=<device address hex>:<entries> (tools/k3_trace.py).

@@ -140,6 +140,11 @@ struct PairParams {
   // of them accumulate exactly in FP32 (group_max * kb * 2^(2(53-rho)) <= 2^24) and
   // the FP64 epilogue runs once per group.  1 = one pair per epilogue pass (reference).
   int group_max;
+  // 1: exclusive epilogue windows — the MMA warp starts a pair only after the
+  // epilogue has finished the previous one, so the FP64 adds never run while the
+  // tensor pipe streams (where they are held back) and the MMAs never run while
+  // the adds do.  0: overlapped (up to kAccBufs accumulators in flight).
+  int serial;
   unsigned long long* trace; // diagnostics (OZ_DIAGNOSTICS builds only): per-pair timestamps of unit 0
   int trace_cap;             // entries (pairs) the trace holds
   // Diagnostics only (OZ_DIAGNOSTICS builds, OZ_DEBUG_MODE): bit 0 = epilogue skips the
@@ -669,6 +674,10 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
           long long full_wait = 0;
           if (tr && lane == 0) P.trace[acc_it * 8 + 0] = clock64();
           if (acc_it >= (uint32_t)kAccBufs) mbar_wait(&s.acc_empty[buf], ((acc_it / kAccBufs) - 1) & 1);
+          if (P.serial && acc_it >= 1 && kAccBufs > 1) {
+            const uint32_t prev = (acc_it - 1) % kAccBufs;
+            mbar_wait(&s.acc_empty[prev], ((acc_it - 1) / kAccBufs) & 1);
+          }
           if (tr && lane == 0) P.trace[acc_it * 8 + 1] = clock64();
           tc_fence_after();
           const uint32_t d_tmem = tmem + buf * kN;
@@ -763,29 +772,30 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
         const bool tr = OZ_DIAGNOSTICS && P.trace && unit == 0 && crank == 0 && warp == 4 && lane == 0 &&
                          acc_it < (uint32_t)P.trace_cap;
         if (tr) P.trace[acc_it * 8 + 3] = clock64();
+        // This pair's exponents are loaded before waiting for its accumulator, so
+        // their latency overlaps the MMAs (short pairs are epilogue-latency-bound).
+        const int ea = (row < P.m && p < lp) ? __ldg(P.expo_a + (int64_t)p * P.m + row) : 0;
+        // Non-zero G has its FP32 exponent field in [g_lo, g_hi] (PairParams).
+        const int2 mm = __ldg(reinterpret_cast<const int2*>(P.ebmm) + (int64_t)q * P.tiles_n + tn);
+        const int32_t* ebq = P.ebsh + (int64_t)q * P.n_pad + tn * kN;
+        // Pull this pair's B-exponent lines into L1 now: the loads that use them
+        // come after the first DADD, i.e. in the short window in which the
+        // epilogue's DADDs can drain, where an L2 miss would stall.
+        constexpr int kRegLines = (kRegHalf + 31) / 32;  // 128-byte lines of this thread's register-part exponents
+        if (lane < kRegLines + (kTmHalf * 4 + 127) / 128) {
+          const int32_t* pf = lane < kRegLines ? ebq + half * kRegHalf + lane * 32 : ebq + kRegCols + half * kTmHalf;
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(pf));
+        }
         mbar_wait(&s.acc_full[buf], (acc_it / kAccBufs) & 1);
         if (tr) P.trace[acc_it * 8 + 4] = clock64();
         tc_fence_after();
         // p >= lp: this CTA's rows have an all-zero A slice p (the partner needs it):
         // the term is +0, nothing to add.
         if (p < lp && !(OZ_DIAGNOSTICS && (P.debug & 1))) {
-          const int ea = row < P.m ? __ldg(P.expo_a + (int64_t)p * P.m + row) : 0;
           const int ea_sh = (ea + 896) * (1 << 20);
-          // Non-zero G has its FP32 exponent field in [g_lo, g_hi] (PairParams).
-          const int2 mm = __ldg(reinterpret_cast<const int2*>(P.ebmm) + (int64_t)q * P.tiles_n + tn);
           // (FMA terms also need the scale 2^(eA+eB) itself normal.)
           const bool safe = ea + 896 + mm.x + P.g_lo >= 1 && ea + 896 + mm.y + P.g_hi <= 2046 &&
                             (kEmu || !OZ_TERM_FMA || (ea + 1023 + mm.x >= 1 && ea + 1023 + mm.y <= 2046));
-          const int32_t* ebq = P.ebsh + (int64_t)q * P.n_pad + tn * kN;
-          // Pull this pair's B-exponent lines into L1 now: the loads that use them
-          // come after the first DADD, i.e. in the short window in which the
-          // epilogue's DADDs can drain, where an L2 miss would stall.
-          constexpr int kRegLines = (kRegHalf + 31) / 32;  // 128-byte lines of this thread's register-part exponents
-          if (lane < kRegLines + (kTmHalf * 4 + 127) / 128) {
-            const int32_t* pf = lane < kRegLines ? ebq + half * kRegHalf + lane * 32
-                                                               : ebq + kRegCols + half * kTmHalf;
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(pf));
-          }
           const uint32_t gaddr = tmem + lane_base + buf * kN;
           auto tmem_part = [&]() {
             // Integer adds (kTmInt): rolled, so the code stays in the instruction cache.
