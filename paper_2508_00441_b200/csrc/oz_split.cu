@@ -270,7 +270,8 @@ OZ_DEVICE uint32_t slice_iteration(uint64_t (&x)[kEPT], const uint64_t sigma, co
 }
 
 template <int kThreads, int kEPT, int kCL, int kEB, bool kEmu>
-__global__ void __launch_bounds__(kThreads, kThreads <= 256 ? 2 : 1) split_fused_kernel(const FusedSplitParams P) {
+// Two CTAs per SM when a CTA holds <= 8192 elements (64 registers per thread at 512 threads).
+__global__ void __launch_bounds__(kThreads, kThreads * kEPT <= 8192 ? 2 : 1) split_fused_kernel(const FusedSplitParams P) {
   constexpr int kV = 16 / kEB;          // elements per 16-byte plane store
   constexpr int kChunks = kEPT / kV;
   constexpr int kWarps = kThreads / 32;
@@ -629,7 +630,7 @@ OZ_DEVICE int col_slice_planes(const ColSplitParams& P, uint64_t (&x)[16], int c
 }
 
 template <int kEB, bool kEmu>
-__global__ void __launch_bounds__(256) col_slice_kernel(const ColSplitParams P) {
+__global__ void __launch_bounds__(256, 3) col_slice_kernel(const ColSplitParams P) {  // >= 3 CTAs (24 warps) per SM
   __shared__ uint64_t tile[kColTK * kColTJ];  // element (k, j) at k*16 + (j ^ (k >> 4 & 15))
   extern __shared__ uint32_t tbl[];
   const int t = threadIdx.x;
