@@ -192,6 +192,12 @@ int oz_set_pair_variant(int cta_group, int tile_n, int raster_group);
  * profiles/epi12_ab_r02.txt). */
 int oz_set_epilogue_warps(int warps);
 
+/* Tuning knob (results are identical): pair-GEMM schedule — 0 overlapped
+ * epilogue (default: up to 2-4 accumulators in flight), 1 exclusive epilogue
+ * windows (the MMA warp starts a pair only after the epilogue finished the
+ * previous one). */
+int oz_set_pair_schedule(int mode);
+
 /* One slice-pair product D (m x n, fp32) = A (m x k) . B (n x k)^T on tcgen05 —
  * replaces lpgemm.lp_gemm (lpgemm.py:93-120) for slice operands (exact). */
 int oz_lp_gemm(const void* a_plane, const void* b_plane, int64_t ld_a, int64_t ld_b, int64_t m, int64_t n,
