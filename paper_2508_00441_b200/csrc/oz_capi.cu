@@ -249,7 +249,8 @@ std::atomic<int> g_epi_warps{8};
 // Pair-GEMM schedule: 0 overlapped epilogue, 1 exclusive epilogue windows.
 std::atomic<int> g_pair_sched{0};
 
-PairPlan plan_pair(int64_t m, int64_t n, int64_t kb, int elem_bytes, int sx, int sy, int pair_cutoff, int emu) {
+PairPlan plan_pair(int64_t m, int64_t n, int64_t kb, int elem_bytes, int sx, int sy, int pair_cutoff, int emu,
+                   bool wide_ok = false) {
   PairPlan pl{};
   // CTA pair (cta_group::2) unless the problem has a single 128-row slab; N = 192
   // columns per pair tile in hardware-FP64 mode (tensor-bound), N = 128 in the
@@ -268,11 +269,15 @@ PairPlan plan_pair(int64_t m, int64_t n, int64_t kb, int elem_bytes, int sx, int
     const int64_t sms = num_sms();
     const bool short_fp8 = elem_bytes == 1 && kb <= 2048 && !emu;
     struct Cand { int cta, tn; double eff; };
-    const Cand cands[4] = {{2, 192, 1.0}, {2, 128, 0.92}, {1, 128, short_fp8 ? 1.10 : 0.935}, {1, 64, 0.795}};
+    // 256 x 256 CTA-pair tiles (Cb partly in C itself): fixed-step grouped mode,
+    // first k-block, hardware FP64 only (wide_ok).
+    const Cand cands[5] = {{2, 256, 1.04}, {2, 192, 1.0}, {2, 128, 0.92}, {1, 128, short_fp8 ? 1.10 : 0.935},
+                           {1, 64, 0.795}};
     double best = 0.0;
     pl.cta = 0;
     for (const Cand& c : cands) {
       if (c.tn == 192 && emu) continue;
+      if (c.tn == 256 && !wide_ok) continue;
       if (c.cta == 2 && m <= oz::kPM) continue;
       if (force_cta && c.cta != (force_cta == 1 ? 1 : 2)) continue;
       if (force_tn && c.tn != force_tn) continue;
@@ -338,9 +343,12 @@ int64_t oz_pair_gemm_workspace(int64_t m, int64_t n, int64_t kb, int type2, int 
   uint32_t idf;
   if (!fmt_info(type2, f, idf)) return 0;
   const PairPlan p0 = plan_pair(m, n, kb, f.bytes, sx, sy, pair_cutoff, 0),
-                 p1 = plan_pair(m, n, kb, f.bytes, sx, sy, pair_cutoff, 1);
-  const size_t b0 = p0.eb_bytes + p0.band_bytes + p0.pace_bytes, b1 = p1.eb_bytes + p1.band_bytes + p1.pace_bytes;
-  return (int64_t)(b0 > b1 ? b0 : b1);
+                 p1 = plan_pair(m, n, kb, f.bytes, sx, sy, pair_cutoff, 1),
+                 p2 = plan_pair(m, n, kb, f.bytes, sx, sy, pair_cutoff, 0, true);
+  const size_t b0 = p0.eb_bytes + p0.band_bytes + p0.pace_bytes, b1 = p1.eb_bytes + p1.band_bytes + p1.pace_bytes,
+               b2 = p2.eb_bytes + p2.band_bytes + p2.pace_bytes;
+  const size_t b01 = b0 > b1 ? b0 : b1;
+  return (int64_t)(b01 > b2 ? b01 : b2);
 }
 
 int oz_split_fused(const double* X, int64_t rows, int64_t kb, int64_t ldx, int type2, int rho, int emu, int cap,
@@ -445,7 +453,7 @@ int oz_split_pad(void* coeff, int64_t ld_coeff, int64_t rows, int type2, int s, 
 }
 
 int oz_set_pair_variant(int cta_group, int tile_n, int raster_group) {
-  if (cta_group < 0 || cta_group > 2 || (tile_n != 0 && tile_n != 64 && tile_n != 128 && tile_n != 192) ||
+  if (cta_group < 0 || cta_group > 2 || (tile_n != 0 && tile_n != 64 && tile_n != 128 && tile_n != 192 && tile_n != 256) ||
       raster_group < 0)
     return OZ_EINVAL;
   g_force_cta.store(cta_group, std::memory_order_relaxed);
@@ -564,7 +572,7 @@ static int pair_gemm_impl(const void* a_planes, const void* b_planes, int64_t ld
   P.order = order; P.cutoff = pair_cutoff; P.accumulate = accumulate;
   P.elem_bytes = f.bytes; P.fmt = idf; P.flags = flags; P.s_dev = s_dev;
   P.fp6 = (type2 == OZ_FMT_E3M2 || type2 == OZ_FMT_E2M3) ? 1 : 0;
-  const PairPlan pl = plan_pair(m, n, kb, f.bytes, sx, sy, pair_cutoff, emu);
+  const PairPlan pl = plan_pair(m, n, kb, f.bytes, sx, sy, pair_cutoff, emu, group_max > 1 && !accumulate);
   const int cta = pl.cta, tn = pl.tn;
   if (!workspace || (size_t)workspace_bytes < pl.eb_bytes) return OZ_EINVAL;  // see oz_pair_gemm_workspace
   P.group = pl.group;
@@ -652,6 +660,8 @@ static int pair_gemm_impl(const void* a_planes, const void* b_planes, int64_t ld
     rc = emu ? launch_pair_fmt<true, 1, 64>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 1, 64>(ma, mb, P, tiles, st);
   else if (cta == 1)
     rc = emu ? launch_pair_fmt<true, 1, 128>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 1, 128>(ma, mb, P, tiles, st);
+  else if (tn == 256)  // fixed-step grouped mode, first k-block, hardware mode (plan_pair)
+    rc = launch_pair_fmt<false, 2, 256>(ma, mb, P, tiles, st);
   else if (tn == 192)  // hardware mode only (plan_pair)
     rc = g_epi_warps.load(std::memory_order_relaxed) == 12 ? launch_pair_fmt<false, 2, 192, 12>(ma, mb, P, tiles, st)
                                                            : launch_pair_fmt<false, 2, 192, 8>(ma, mb, P, tiles, st);

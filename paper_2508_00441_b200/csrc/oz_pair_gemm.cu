@@ -33,6 +33,12 @@
 #ifndef OZ_TERM_FMA
 #define OZ_TERM_FMA 1  // HW-mode safe terms: DFMA(double(G), 2^(eA+eB), Cb) instead of bit assembly + DADD
 #endif
+#ifndef OZ_GLB_REG
+#define OZ_GLB_REG 128  // N = 256: Cb columns kept in registers (the rest read-modify-written in C)
+#endif
+#ifndef OZ_GLB_INT
+#define OZ_GLB_INT 1  // N = 256: C-resident half of Cb added with integer add_lean, before the DFMA half
+#endif
 #ifndef OZ_HW_INT_TMEM
 #define OZ_HW_INT_TMEM 0  // 1: hardware mode adds the TMEM third of Cb with integer add_lean, first (A/B: slower)
 #endif
@@ -72,15 +78,21 @@ struct PairCfg {
   static constexpr int kParts = kEpi / 4;                     // epilogue threads per C row
   static constexpr int kBRows = kN / kCta;                    // B rows staged per CTA
   static constexpr int kStageBytes = (kPM + kBRows) * 128;    // per CTA
-  static constexpr int kRegCols = kEmu ? 0 : (kEpi == 12 ? kN * 3 / 4 : (kN < 128 ? kN : 128));  // Cb cols in registers
+  static constexpr int kRegCols =
+      kEmu ? 0 : (kN == 256 ? OZ_GLB_REG : (kEpi == 12 ? kN * 3 / 4 : (kN < 128 ? kN : 128)));  // Cb cols in registers
   static constexpr int kRegHalf = kRegCols / kParts;          // ... per epilogue thread
   static constexpr int kAccBufs = kN == 64 ? 4 : ((kEmu || kN != 128) ? 2 : 4);
-  static constexpr int kTmCols = kN - kRegCols;               // C columns whose Cb lives in TMEM
+  // N = 256 (fixed-step grouped mode, single k-block): both accumulators fill TMEM,
+  // so the Cb columns beyond the register part live in C itself (global memory,
+  // read-modify-written once per pair group — 16 times per tile at cutoff 11).
+  static constexpr int kTmCols = kN == 256 ? 0 : kN - kRegCols;  // C columns whose Cb lives in TMEM
+  static constexpr int kGlbCols = kN - kRegCols - kTmCols;    // C columns whose Cb lives in C (N = 256)
   static constexpr int kCbTmem = kAccBufs * kN;               // first TMEM column of that Cb
   static constexpr int kSmemBudget = 227 * 1024 - 2048;
   static constexpr int kStages = kSmemBudget / kStageBytes > 10 ? 10 : kSmemBudget / kStageBytes;
   static_assert(kCbTmem + 2 * kTmCols <= kTmemCols, "TMEM budget");
   static_assert(kN <= 128 || kCta == 2, "N > 128 needs the CTA pair");
+  static_assert(kGlbCols == 0 || (kN == 256 && !kEmu && kEpi == 8), "global Cb: N = 256 hardware mode only");
   static_assert(kRegHalf % 16 == 0 && (kN - kRegCols) % (16 * kParts) == 0, "16-column TMEM chunks per thread");
   static_assert(kEpi == 8 || (kEpi == 12 && !kEmu), "12 epilogue warps: hardware FP64 mode only");
   static constexpr int kRegLo = 40;                           // setmaxnreg: producer / MMA warps
@@ -479,6 +491,27 @@ OZ_DEVICE void accumulate16(const uint32_t (&g)[16], const int32_t* eb_sh, int e
   for (int j = 0; j < 16; ++j) cb[j] = d2u(__dadd_rn(u2d(cb[j]), u2d(t[j])));
 }
 
+// Cb[16] = C[row, col0 : col0+16] when `init` (the tile's C-resident Cb columns
+// hold its running sum), else +0; columns past n and rows past m read as +0.
+OZ_DEVICE void glb_load16(const PairParams& P, int row, int col0, bool init, uint64_t (&c)[16]) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) c[j] = 0ull;
+  if (!init || row >= P.m) return;
+  const uint64_t* crow = reinterpret_cast<const uint64_t*>(P.C) + (int64_t)row * P.ldc + col0;
+  if (((reinterpret_cast<uintptr_t>(crow) & 15) == 0) && col0 + 16 <= P.n) {
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) {
+      const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(crow + j);
+      c[j] = v.x;
+      c[j + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (col0 + j < P.n) c[j] = crow[j];
+  }
+}
+
 // C[row, col0 : col0+cnt] = Cb (first block) or C + Cb (ozgemm.py:204-207).
 template <bool kEmu, typename Acc>
 OZ_DEVICE void store_row(const PairParams& P, int row, int col0, const Acc* cb, int cnt, uint32_t& flags) {
@@ -719,10 +752,12 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
     // ───────── epilogue: ordered FP64 accumulation ─────────
     constexpr int kRegCols = Cfg::kRegCols;
     constexpr int kTmHalf = Cfg::kTmCols / Cfg::kParts;  // TMEM-resident Cb columns per thread
+    constexpr int kGlbHalf = Cfg::kGlbCols / Cfg::kParts;  // C-resident Cb columns per thread (N = 256)
     // TMEM-resident Cb with integer adds (always in emulated mode; hardware mode:
     // OZ_HW_INT_TMEM), processed before the register part.
     constexpr bool kTmInt = kEmu || OZ_HW_INT_TMEM;
     constexpr bool kTmFirst = !kEmu && OZ_HW_INT_TMEM;
+    constexpr bool kGlbInt = OZ_GLB_INT != 0;  // N = 256: C-resident Cb via integer add_lean, first
     const int quad = warp & 3;               // TMEM lane quadrant this warp may access
     constexpr int kRegHalf = Cfg::kRegHalf;
     const int half = (warp - kLeadWarps) >> 2;        // part: register Cb cols [kRegHalf h, +kRegHalf); TMEM Cb: [kRegCols + kTmHalf*h, +kTmHalf)
@@ -753,6 +788,7 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
         tmem_st_wait();
       }
 
+      bool glb_init = false;  // N = 256: this tile's C-resident Cb columns written yet
       PairIter pi;
       pi.init(lp_walk, lq, P.order, P.cutoff);
       for (; pi.valid(); ++acc_it) {
@@ -782,8 +818,10 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
         // come after the first DADD, i.e. in the short window in which the
         // epilogue's DADDs can drain, where an L2 miss would stall.
         constexpr int kRegLines = (kRegHalf + 31) / 32;  // 128-byte lines of this thread's register-part exponents
-        if (lane < kRegLines + (kTmHalf * 4 + 127) / 128) {
-          const int32_t* pf = lane < kRegLines ? ebq + half * kRegHalf + lane * 32 : ebq + kRegCols + half * kTmHalf;
+        constexpr int kOtherLines = (kTmHalf * 4 + 127) / 128 + (kGlbHalf * 4 + 127) / 128;
+        if (lane < kRegLines + kOtherLines) {
+          const int32_t* pf = lane < kRegLines ? ebq + half * kRegHalf + lane * 32
+                                               : ebq + kRegCols + half * (kTmHalf + kGlbHalf) + (lane - kRegLines) * 32;
           asm volatile("prefetch.global.L1 [%0];" ::"l"(pf));
         }
         mbar_wait(&s.acc_full[buf], (acc_it / kAccBufs) & 1);
@@ -822,6 +860,26 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
             }
             tmem_st_wait();
           };
+          auto glb_part = [&]() {
+            // C-resident part (N = 256, first k-block only): Cb = C[row, cols] (+0
+            // before this tile's first group), Cb += T, C[row, cols] = Cb.  OZ_GLB_INT:
+            // integer add_lean (issued before the register part's DFMAs, so it is not
+            // held back behind them; bit-identical).
+            const int col0 = tn * kN + kRegCols + half * kGlbHalf;
+#pragma unroll(kGlbInt || kGlbHalf < 16 ? 1 : kGlbHalf / 16)
+            for (int ch = 0; ch < kGlbHalf / 16; ++ch) {
+              uint32_t g[16];
+              tmem_ld16(gaddr + kRegCols + half * kGlbHalf + ch * 16, g);
+              uint64_t c16[16];
+              glb_load16(P, row, col0 + ch * 16, glb_init, c16);
+              tmem_ld_wait_regs(g);
+              accumulate16<kEmu, kGlbInt>(g, ebq + kRegCols + half * kGlbHalf + ch * 16, ea_sh, safe, c16,
+                                                   flags);
+              if (row < P.m) store_row<kEmu>(P, row, col0 + ch * 16, c16, 16, flags);
+            }
+            glb_init = true;
+          };
+          if constexpr (kGlbHalf > 0 && kGlbInt) glb_part();
           // Hardware mode, integer TMEM part: issued first, while the tensor pipe runs
           // (integer ops are not held back by the MMAs; the register part's DFMAs are).
           if constexpr (kTmHalf > 0 && kTmFirst) tmem_part();
@@ -841,6 +899,7 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
           }
           if (tr) P.trace[acc_it * 8 + 7] = clock64();
           if constexpr (kTmHalf > 0 && !kTmFirst) tmem_part();
+          if constexpr (kGlbHalf > 0 && !kGlbInt) glb_part();
         }
         tc_fence_before();
         __syncwarp();
@@ -854,6 +913,16 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
       // C = Cb (first block) or C = C + Cb (ozgemm.py:204-207).  The TMEM reads
       // are warp-collective (.sync.aligned): issue them outside the row guard.
       const bool store = !(OZ_DIAGNOSTICS && (P.debug & 8));  // diagnostics: bit 3 skips the C stores
+      if constexpr (kGlbHalf > 0) {
+        if (!glb_init && row < P.m && store) {  // every group skipped (all-zero A slices): Cb = +0
+          uint64_t z[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) z[j] = 0ull;
+#pragma unroll
+          for (int ch = 0; ch < kGlbHalf / 16; ++ch)
+            store_row<kEmu>(P, row, tn * kN + kRegCols + half * kGlbHalf + ch * 16, z, 16, flags);
+        }
+      }
       if constexpr (kRegCols > 0)
         if (row < P.m && store) store_row<kEmu>(P, row, tn * kN + half * kRegHalf, cb, kRegHalf, flags);
       if constexpr (kTmHalf > 0) {

@@ -276,7 +276,7 @@ FIXED_CASES = [
 
 @pytest.mark.parametrize("case", FIXED_CASES, ids=[f"{c[0]}x{c[1]}x{c[2]}-{c[4]}-kb{c[5]}-emu{int(c[6])}"
                                                    f"-ms{c[7]}-{c[8][:5]}-cut{c[9]}" for c in FIXED_CASES])
-@pytest.mark.parametrize("variant", [("1", "64"), ("1", "128"), ("2", "128"), ("2", "192")],
+@pytest.mark.parametrize("variant", [("1", "64"), ("1", "128"), ("2", "128"), ("2", "192"), ("2", "256")],
                          ids=lambda v: f"cta{v[0]}-n{v[1]}")
 def test_fixed_step_grouped_bitwise(cuda, case, variant, pair_variant):
     """slice_exponents="fixed" (opt-in): fixed-step slices and level-grouped
@@ -465,3 +465,28 @@ def test_variants_agree_multiwave(cuda, kw, pair_variant):
             ref = C.clone()
         else:
             assert torch.equal(C.view(torch.int64), ref.view(torch.int64)), (cta, tn)
+
+
+@pytest.mark.parametrize("shape", [(1100, 1300, 1000), (600, 515, 333)], ids=["multiwave", "ragged"])
+def test_fixed_step_wide_tiles_bitwise(cuda, shape, pair_variant):
+    """256 x 256 CTA-pair tiles (fixed-step grouped mode; half of Cb read-modify-
+    written in C itself): bitwise the CPU restatement over several tile waves,
+    ragged edges, and 128-row slabs whose A slices are all zero (every group
+    of that CTA skipped: its C-resident columns must still be written as +0)."""
+    import oracle
+
+    pair_variant(2, 256)
+    oz = _oz()
+    m, n, k = shape
+    rng = np.random.default_rng(m + n + k)
+    A = spread_matrix(rng, m, k, 1.0)
+    A[128:256] = 0.0  # one whole 128-row slab of zeros
+    A[300, :] *= 2.0 ** 40
+    B = spread_matrix(rng, k, n, 1.0)
+    for cut in (11, 6):
+        cfg = oz.GemmConfig(oz.get_format("fp8e4m3"), oz.get_format("fp32"), pair_cutoff=cut,
+                            slice_exponents="fixed")
+        res = oz.oz_gemm(A, B, cfg)
+        Cref, _ = oracle.oz_gemm_fixed(A, B, "fp8e4m3", "fp32", 0, None, "smallest-first", cut)
+        nbad = int(np.sum(bits(res.C) != bits(Cref)))
+        assert nbad == 0, f"cut {cut}: {nbad}/{m * n} entries differ"

@@ -20,11 +20,16 @@ ap.add_argument("--pair-cutoff", type=int, default=None)
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--fixed", action="store_true", help="slice_exponents='fixed'")
 ap.add_argument("--kblock", type=int, default=0)
+ap.add_argument("--variant", type=int, nargs=2, default=None, metavar=("CTA", "N"), help="force the pair-GEMM variant")
 a = ap.parse_args()
 A, _ = gpu_inputs(torch, a.n, a.n, 8, a.phi, 1000, "cuda")
 _, B = gpu_inputs(torch, 8, a.n, a.n, a.phi, 2000, "cuda")
 cfg = oz.GemmConfig(oz.get_format(a.type2), oz.get_format("fp32"), fp64_emulation=a.emu, pair_cutoff=a.pair_cutoff,
                     k_block=a.kblock, slice_exponents="fixed" if a.fixed else "adaptive")
+if a.variant:
+    from paper_2508_00441_b200 import _lib
+
+    _lib.set_pair_variant(a.variant[0], a.variant[1], 0)
 for _ in range(a.reps):
     C, st = oz.oz_gemm_device(A, B, cfg)
 torch.cuda.synchronize()
