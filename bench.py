@@ -368,13 +368,13 @@ def main():
     fp8_peak = 2.0 * peaks["bf16"]
     achieved = mma_flops / (gemm_ms / 1e3) / 1e12
     traffic = None
-    prof = ROOT / "profiles" / "pair_gemm_r02_defaults_summary.json"
+    prof = ROOT / "profiles" / "pair_gemm_r02_defaults_final_summary.json"
     if prof.exists() and args.n == 8192 and args.pair_cutoff is None and args.type2 == "fp8e4m3" and not args.kblock:
         traffic = json.loads(prof.read_text())["traffic_bytes_per_launch"]  # ncu --set full, same workload
     roofline = {"bound": "tensor", "achieved": achieved, "peak": fp8_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp8_peak, "traffic": traffic,
                 "traffic_source": "dram read+write per launch, ncu --set full of this workload, "
-                                  "profiles/pair_gemm_r02_defaults_summary.json"
+                                  "profiles/pair_gemm_r02_defaults_final_summary.json"
                 if traffic else None,
                 "kernel": "pair_gemm_kernel<false> (fused slice-pair GEMM + FP64 accumulation)",
                 "peak_source": f"dense fp8 = 2 x measured dense bf16 ({peaks['source']})",

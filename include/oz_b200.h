@@ -192,6 +192,14 @@ int oz_set_pair_variant(int cta_group, int tile_n, int raster_group);
  * profiles/epi12_ab_r02.txt). */
 int oz_set_epilogue_warps(int warps);
 
+/* Host-only query: the pair-GEMM kernel variant oz_pair_gemm / oz_pair_gemm_grouped
+ * would launch for these sizes and options (wave-cost model, oz_set_pair_variant
+ * overrides applied): *cta_group in {1, 2}, *tile_n in {64, 128, 192, 256}.  The
+ * emulated mode (emu = 1) only ever gets variants that have an integer-only
+ * instantiation (tile_n 64 or 128). */
+int oz_pair_plan(int64_t m, int64_t n, int64_t kb, int type2, int sx, int sy, int pair_cutoff, int emu, int group_max,
+                 int accumulate, int* cta_group, int* tile_n);
+
 /* Tuning knob (results are identical): pair-GEMM schedule — 0 overlapped
  * epilogue (default: up to 2-4 accumulators in flight), 1 exclusive epilogue
  * windows (the MMA warp starts a pair only after the epilogue finished the

@@ -54,6 +54,7 @@ SIGNATURES = {
     "oz_set_pair_variant": (_I, [_I, _I, _I]),
     "oz_set_epilogue_warps": (_I, [_I]),
     "oz_set_pair_schedule": (_I, [_I]),
+    "oz_pair_plan": (_I, [_I64, _I64, _I64, _I, _I, _I, _I, _I, _I, _I, _P, _P]),
     "oz_lp_gemm": (_I, [_P, _P, _I64, _I64, _I64, _I64, _I64, _I, _P, _I64, _P]),
     "oz_emu_add_batch": (_I, [_P, _P, _P, _I64, _I, _P, _P]),
     "oz_dd_gemm": (_I, [_P, _P, _P, _I64, _I64, _I64, _P]),

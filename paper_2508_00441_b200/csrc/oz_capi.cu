@@ -277,7 +277,7 @@ PairPlan plan_pair(int64_t m, int64_t n, int64_t kb, int elem_bytes, int sx, int
     pl.cta = 0;
     for (const Cand& c : cands) {
       if (c.tn == 192 && emu) continue;
-      if (c.tn == 256 && !wide_ok) continue;
+      if (c.tn == 256 && (!wide_ok || emu)) continue;  // hardware-FP64 grouped kernel only
       if (c.cta == 2 && m <= oz::kPM) continue;
       if (force_cta && c.cta != (force_cta == 1 ? 1 : 2)) continue;
       if (force_tn && c.tn != force_tn) continue;
@@ -459,6 +459,18 @@ int oz_set_pair_variant(int cta_group, int tile_n, int raster_group) {
   g_force_cta.store(cta_group, std::memory_order_relaxed);
   g_force_tn.store(tile_n, std::memory_order_relaxed);
   g_force_group.store(raster_group, std::memory_order_relaxed);
+  return OZ_OK;
+}
+
+int oz_pair_plan(int64_t m, int64_t n, int64_t kb, int type2, int sx, int sy, int pair_cutoff, int emu, int group_max,
+                 int accumulate, int* cta_group, int* tile_n) {
+  LpFormat f;
+  uint32_t idf;
+  if (!fmt_info(type2, f, idf)) return OZ_EUNSUPPORTED;
+  if (m <= 0 || n <= 0 || kb <= 0 || sx < 0 || sy < 0 || !cta_group || !tile_n) return OZ_EINVAL;
+  const PairPlan pl = plan_pair(m, n, kb, f.bytes, sx, sy, pair_cutoff, emu, group_max > 1 && !accumulate);
+  *cta_group = pl.cta;
+  *tile_n = pl.tn;
   return OZ_OK;
 }
 
@@ -660,8 +672,10 @@ static int pair_gemm_impl(const void* a_planes, const void* b_planes, int64_t ld
     rc = emu ? launch_pair_fmt<true, 1, 64>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 1, 64>(ma, mb, P, tiles, st);
   else if (cta == 1)
     rc = emu ? launch_pair_fmt<true, 1, 128>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 1, 128>(ma, mb, P, tiles, st);
-  else if (tn == 256)  // fixed-step grouped mode, first k-block, hardware mode (plan_pair)
+  else if (tn == 256 && !emu)  // fixed-step grouped mode, first k-block, hardware mode (plan_pair)
     rc = launch_pair_fmt<false, 2, 256>(ma, mb, P, tiles, st);
+  else if (tn == 256)
+    return OZ_EINVAL;  // never planned: the emulated mode has no 256-column kernel
   else if (tn == 192)  // hardware mode only (plan_pair)
     rc = g_epi_warps.load(std::memory_order_relaxed) == 12 ? launch_pair_fmt<false, 2, 192, 12>(ma, mb, P, tiles, st)
                                                            : launch_pair_fmt<false, 2, 192, 8>(ma, mb, P, tiles, st);

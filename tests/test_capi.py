@@ -131,3 +131,32 @@ def test_pair_gemm_workspace_query_without_gpu(lib):
     small = lib.oz_pair_gemm_workspace(256, 192, 256, 0, 4, 4, -1)
     assert small > 0 and small % 4 == 0
     assert lib.oz_pair_gemm_workspace(8192, 8192, 8192, 0, 16, 17, -1) > lib.oz_pair_gemm_workspace(8192, 8192, 8192, 0, 16, 17, 11)
+
+
+def test_pair_plan_emulated_mode_never_gets_a_hardware_kernel(lib):
+    """The emulated-FP64 mode must only launch integer-only instantiations (no
+    N = 192 / 256 kernel exists for it): the host plan never picks them, for any
+    size, k-block, grouping or forced variant; the hardware grouped mode gets
+    the 256-column tiles at large n."""
+    import ctypes
+
+    cta, tn = ctypes.c_int(), ctypes.c_int()
+
+    def plan(m, n, kb, emu, gmax=1, acc=0, t2=0):
+        assert lib.oz_pair_plan(m, n, kb, t2, 16, 16, -1, emu, gmax, acc, ctypes.byref(cta), ctypes.byref(tn)) == 0
+        return cta.value, tn.value
+
+    try:
+        for forced in ((0, 0), (2, 192), (2, 256), (1, 64), (1, 128)):
+            assert lib.oz_set_pair_variant(forced[0], forced[1], 0) == 0
+            for n in (256, 1024, 2048, 4096, 8192, 16384):
+                for kb in (256, 1024, 8192):
+                    for gmax, acc in ((1, 0), (8, 0), (8, 1)):
+                        c, t = plan(n, n, kb, 1, gmax, acc)
+                        assert t in (64, 128), (forced, n, kb, gmax, acc, c, t)
+    finally:
+        lib.oz_set_pair_variant(0, 0, 0)
+    assert plan(8192, 8192, 8192, 0, 8, 0) == (2, 256)
+    assert plan(8192, 8192, 8192, 0, 1, 0) == (2, 192)
+    assert plan(8192, 8192, 8192, 0, 8, 1)[1] != 256  # later k-blocks accumulate into C: no C-resident Cb
+    assert plan(1024, 1024, 1024, 0) == (1, 64)
