@@ -196,7 +196,7 @@ int oz_set_epilogue_warps(int warps);
  * would launch for these sizes and options (wave-cost model, oz_set_pair_variant
  * overrides applied): *cta_group in {1, 2}, *tile_n in {64, 128, 192, 256}.  The
  * emulated mode (emu = 1) only ever gets variants that have an integer-only
- * instantiation (tile_n 64 or 128). */
+ * instantiation (tile_n 64, 128, or 256 in grouped mode). */
 int oz_pair_plan(int64_t m, int64_t n, int64_t kb, int type2, int sx, int sy, int pair_cutoff, int emu, int group_max,
                  int accumulate, int* cta_group, int* tile_n);
 

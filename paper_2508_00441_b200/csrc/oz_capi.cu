@@ -277,7 +277,7 @@ PairPlan plan_pair(int64_t m, int64_t n, int64_t kb, int elem_bytes, int sx, int
     pl.cta = 0;
     for (const Cand& c : cands) {
       if (c.tn == 192 && emu) continue;
-      if (c.tn == 256 && (!wide_ok || emu)) continue;  // hardware-FP64 grouped kernel only
+      if (c.tn == 256 && !wide_ok) continue;  // grouped mode, first k-block
       if (c.cta == 2 && m <= oz::kPM) continue;
       if (force_cta && c.cta != (force_cta == 1 ? 1 : 2)) continue;
       if (force_tn && c.tn != force_tn) continue;
@@ -672,10 +672,8 @@ static int pair_gemm_impl(const void* a_planes, const void* b_planes, int64_t ld
     rc = emu ? launch_pair_fmt<true, 1, 64>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 1, 64>(ma, mb, P, tiles, st);
   else if (cta == 1)
     rc = emu ? launch_pair_fmt<true, 1, 128>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 1, 128>(ma, mb, P, tiles, st);
-  else if (tn == 256 && !emu)  // fixed-step grouped mode, first k-block, hardware mode (plan_pair)
-    rc = launch_pair_fmt<false, 2, 256>(ma, mb, P, tiles, st);
-  else if (tn == 256)
-    return OZ_EINVAL;  // never planned: the emulated mode has no 256-column kernel
+  else if (tn == 256)  // fixed-step grouped mode, first k-block (plan_pair); emulated: all of Cb in C, integer adds
+    rc = emu ? launch_pair_fmt<true, 2, 256>(ma, mb, P, tiles, st) : launch_pair_fmt<false, 2, 256>(ma, mb, P, tiles, st);
   else if (tn == 192)  // hardware mode only (plan_pair)
     rc = g_epi_warps.load(std::memory_order_relaxed) == 12 ? launch_pair_fmt<false, 2, 192, 12>(ma, mb, P, tiles, st)
                                                            : launch_pair_fmt<false, 2, 192, 8>(ma, mb, P, tiles, st);

@@ -92,7 +92,7 @@ struct PairCfg {
   static constexpr int kStages = kSmemBudget / kStageBytes > 10 ? 10 : kSmemBudget / kStageBytes;
   static_assert(kCbTmem + 2 * kTmCols <= kTmemCols, "TMEM budget");
   static_assert(kN <= 128 || kCta == 2, "N > 128 needs the CTA pair");
-  static_assert(kGlbCols == 0 || (kN == 256 && !kEmu && kEpi == 8), "global Cb: N = 256 hardware mode only");
+  static_assert(kGlbCols == 0 || (kN == 256 && kEpi == 8), "C-resident Cb: N = 256 only");
   static_assert(kRegHalf % 16 == 0 && (kN - kRegCols) % (16 * kParts) == 0, "16-column TMEM chunks per thread");
   static_assert(kEpi == 8 || (kEpi == 12 && !kEmu), "12 epilogue warps: hardware FP64 mode only");
   static constexpr int kRegLo = 40;                           // setmaxnreg: producer / MMA warps
@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
     // OZ_HW_INT_TMEM), processed before the register part.
     constexpr bool kTmInt = kEmu || OZ_HW_INT_TMEM;
     constexpr bool kTmFirst = !kEmu && OZ_HW_INT_TMEM;
-    constexpr bool kGlbInt = OZ_GLB_INT != 0;  // N = 256: C-resident Cb via integer add_lean, first
+    constexpr bool kGlbInt = kEmu || OZ_GLB_INT != 0;  // N = 256: C-resident Cb via integer add_lean, first
     const int quad = warp & 3;               // TMEM lane quadrant this warp may access
     constexpr int kRegHalf = Cfg::kRegHalf;
     const int half = (warp - kLeadWarps) >> 2;        // part: register Cb cols [kRegHalf h, +kRegHalf); TMEM Cb: [kRegCols + kTmHalf*h, +kTmHalf)

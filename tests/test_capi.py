@@ -98,8 +98,8 @@ def is_emulated_path_kernel(name: str) -> bool:
 
 def test_emulated_kernels_have_no_fp64_arithmetic(lib):
     """north_star: the emulated path contains no DFMA/DADD/DMUL (or any other
-    FP64 instruction) in its SASS — checked over all 24 emulated split / pair-GEMM
-    instantiations (16 row splits, 2 in-place column splits, 6 pair GEMMs) and
+    FP64 instruction) in its SASS — checked over all 28 emulated split / pair-GEMM
+    instantiations (18 row splits, 2 in-place column splits, 8 pair GEMMs) and
     the 7 helpers they run with."""
     from paper_2508_00441_b200 import _lib
 
@@ -107,7 +107,7 @@ def test_emulated_kernels_have_no_fp64_arithmetic(lib):
     n_split = sum(1 for k in sel if EMU_SPLIT.search(k))
     n_cols = sum(1 for k in sel if EMU_COLS.search(k))
     n_pair = sum(1 for k in sel if "pair_gemm_kernelILb1E" in k)
-    assert n_split == 16 and n_cols == 2 and n_pair == 6, (n_split, n_cols, n_pair)
+    assert n_split == 18 and n_cols == 2 and n_pair == 8, (n_split, n_cols, n_pair)
     assert all(any(h in k for k in sel) for h in EMU_HELPERS)
     for name, lines in sel.items():
         bad = [ln for ln in lines if FP64_OPS.search(ln)]
@@ -135,7 +135,8 @@ def test_pair_gemm_workspace_query_without_gpu(lib):
 
 def test_pair_plan_emulated_mode_never_gets_a_hardware_kernel(lib):
     """The emulated-FP64 mode must only launch integer-only instantiations (no
-    N = 192 / 256 kernel exists for it): the host plan never picks them, for any
+    N = 192 kernel exists for it; N = 256 only in grouped mode, first k-block,
+    where its Cb lives in C): the host plan never picks others, for any
     size, k-block, grouping or forced variant; the hardware grouped mode gets
     the 256-column tiles at large n."""
     import ctypes
@@ -153,7 +154,7 @@ def test_pair_plan_emulated_mode_never_gets_a_hardware_kernel(lib):
                 for kb in (256, 1024, 8192):
                     for gmax, acc in ((1, 0), (8, 0), (8, 1)):
                         c, t = plan(n, n, kb, 1, gmax, acc)
-                        assert t in (64, 128), (forced, n, kb, gmax, acc, c, t)
+                        assert t in (64, 128) or (t == 256 and gmax > 1 and not acc), (forced, n, kb, gmax, acc, c, t)
     finally:
         lib.oz_set_pair_variant(0, 0, 0)
     assert plan(8192, 8192, 8192, 0, 8, 0) == (2, 256)
