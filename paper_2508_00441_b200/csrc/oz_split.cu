@@ -185,13 +185,58 @@ OZ_DEVICE uint64_t emu_slice_elem(uint64_t x, int g, int& k) {
   return (rs << 63) | ((uint64_t)(ef + pos - 52) << 52) | ((rm << (52 - pos)) & kFracMask);
 }
 
+// Fixed-step emulated slicing in fixed point (no renormalisation per plane): an
+// element's residual is kept as |r| in units of ulp(x) (53 bits), its sign, and
+// sh0 = the right shift that puts plane 0's grid q_0 at bit 0 (clamped to 1023;
+// sh0 >= rho - 1 > 0 since |x| <= 2^c0).  Plane p's shift is sh0 + dg with
+// dg = g_p - g_0 = -p w.  k = RNE(r / q_p) and the exact residual are the values
+// emu_slice_elem produces (the reference's three emulated adds), without the
+// FP64 packing: state = rm | sign << 53 | sh0 << 54.
+constexpr uint64_t kFxRm = (1ull << 53) - 1;
+
+OZ_DEVICE uint64_t fx_state(uint64_t x, int g0) {
+  if ((x << 1) == 0) return 0ull;  // +-0: residual 0 (k = 0 for every plane)
+  const int ef = (int)((x >> 52) & 0x7FF);
+  const int sh0 = min(g0 - ef + 1075, 1023);
+  return ((x & kFracMask) | kHidden) | ((x >> 63) << 53) | ((uint64_t)sh0 << 54);
+}
+
+OZ_DEVICE uint64_t fx_slice(uint64_t st, int dg, int& k) {
+  // (A branch-free form with one select was measured slower: 2.7 vs 2.0 ms per
+  // 8192^2 operand; almost all elements take the general branch.)
+  const uint64_t rm = st & kFxRm;
+  const uint32_t sgn = (uint32_t)(st >> 53) & 1u;
+  const int sh = (int)(st >> 54) + dg;
+  uint64_t rm2;
+  uint32_t kk, sg2 = sgn;
+  if (sh <= 0) {          // the residual lies on the grid: it is the whole slice
+    kk = (uint32_t)(rm << min(-sh, 63));
+    rm2 = 0;
+  } else if (sh >= 54) {  // |r| < q / 2 (rm < 2^53): k = 0
+    kk = 0;
+    rm2 = rm;
+  } else {
+    const uint64_t k0 = rm >> sh, rem = rm & ((1ull << sh) - 1), half = 1ull << (sh - 1);
+    const bool up = rem > half || (rem == half && (k0 & 1ull));
+    kk = (uint32_t)k0 + (up ? 1u : 0u);
+    rm2 = up ? 2 * half - rem : rem;
+    sg2 = up ? sgn ^ 1u : sgn;
+  }
+  k = sgn ? -(int)kk : (int)kk;
+  return rm2 == 0 ? (st & ~((1ull << 54) - 1)) : (rm2 | ((uint64_t)sg2 << 53) | (st & ~((1ull << 54) - 1)));
+}
+
+
+
 // One reference iteration over this thread's elements (slicing.py:162-176):
 // returns the next max key.  kWrite: emit the 16-byte plane vectors; kChecked:
 // per-element subnormal-residual and representability checks (only needed for
 // rows holding inputs below 2^-969, or code tables with unrepresentable entries).
 // kKey = false (fixed-step fast path, kWrite only): return the OR of the codes
 // instead of the max key (the row max is not needed there).
-template <int kThreads, int kEPT, int kEB, bool kEmu, bool kWrite, bool kChecked, bool kKey = true>
+// kFx (emulated fixed-step fast path): x[] holds fx_state() words and g is the
+// plane's grid offset dg = g_p - g_0.
+template <int kThreads, int kEPT, int kEB, bool kEmu, bool kWrite, bool kChecked, bool kKey = true, bool kFx = false>
 OZ_DEVICE uint32_t slice_iteration(uint64_t (&x)[kEPT], const uint64_t sigma, const int g, const uint32_t* __restrict__ tblc,
                                    int K, uint8_t* plane, int64_t base, int t, int64_t ld, uint32_t& flags,
                                    uint32_t& bad, const int pack6) {
@@ -206,7 +251,9 @@ OZ_DEVICE uint32_t slice_iteration(uint64_t (&x)[kEPT], const uint64_t sigma, co
       const int i = ch * kV + u;
       uint64_t xn;
       int k;  // slice integer: coeff = k * 2^(rho-53)
-      if constexpr (kEmu && !kChecked) {
+      if constexpr (kFx) {
+        xn = fx_slice(x[i], g, k);
+      } else if constexpr (kEmu && !kChecked) {
         xn = emu_slice_elem(x[i], g, k);
       } else if constexpr (kEmu) {
         const uint64_t xs = emu_add(x[i], sigma, flags);
@@ -379,10 +426,23 @@ __global__ void __launch_bounds__(kThreads, kThreads * kEPT <= 8192 ? 2 : 1) spl
       // entering iteration it is non-zero exactly when a code of an iteration
       // >= it or the final residual is non-zero (count-only mode: the key).
       int z = 0;
+      // Emulated mode, rows without tiny inputs: fixed-point residuals (fx_slice).
+      const bool fx = kEmu && write && !checked && L * P.fixed_w <= 900;
+      if (fx) {
+        const int g0 = c0 + P.rho - 53;
+#pragma unroll
+        for (int i = 0; i < kEPT; ++i) x[i] = fx_state(x[i], g0);
+      }
       for (int it = 0; it < L; ++it) {
         const int c = c0 - it * P.fixed_w;
         const uint64_t sigma = ((uint64_t)(c + P.rho - 1 + 1023) << 52) | (1ull << 51);
         uint8_t* plane = row_plane0 + (int64_t)it * plane_stride;
+        if (kEmu && fx) {
+          const uint32_t cor = slice_iteration<kThreads, kEPT, kEB, kEmu, true, false, false, true>(
+              x, sigma, -it * P.fixed_w, tblc, K, plane, base, t, P.ld, flags, bad, P.pack6);
+          if (cor & 0xFFFFu) z = it + 1;
+          continue;
+        }
         if (!write) {
           if (key != 0) z = it + 1;
           key = slice_iteration<kThreads, kEPT, kEB, kEmu, false, true>(x, sigma, c + P.rho - 53, tblc, K, plane, base,
@@ -401,7 +461,10 @@ __global__ void __launch_bounds__(kThreads, kThreads * kEPT <= 8192 ? 2 : 1) spl
       }
       uint32_t rest = 0;
 #pragma unroll
-      for (int i = 0; i < kEPT; ++i) rest |= (uint32_t)x[i] | ((uint32_t)(x[i] >> 32) << 1);
+      for (int i = 0; i < kEPT; ++i) {
+        const uint64_t r = fx ? (x[i] & kFxRm) : x[i];
+        rest |= (uint32_t)r | ((uint32_t)(r >> 32) << 1);
+      }
       if (rest) z = L + 1;  // still non-zero where a limit check stops the loop
       const int need = (int)row_max((uint32_t)z, 1);
       cnt = min(need, L);
@@ -554,6 +617,12 @@ OZ_DEVICE int col_slice_planes(const ColSplitParams& P, uint64_t (&x)[16], int c
   constexpr int kV = 16 / kEB;
   uint32_t bad = 0;
   int z = 0;
+  // Emulated mode without tiny inputs: fixed-point residuals (fx_slice).
+  const bool fx = kEmu && !kChecked && L * P.w <= 900;
+  if (fx) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) x[u] = fx_state(x[u], c0 + P.rho - 53);
+  }
   for (int it = 0; it < L; ++it) {
     const int c = c0 - it * P.w;
     const int g = c + P.rho - 53;
@@ -565,7 +634,7 @@ OZ_DEVICE int col_slice_planes(const ColSplitParams& P, uint64_t (&x)[16], int c
       uint64_t xn;
       int k;
       if constexpr (kEmu && !kChecked) {
-        xn = emu_slice_elem(x[u], g, k);
+        xn = fx ? fx_slice(x[u], -it * P.w, k) : emu_slice_elem(x[u], g, k);
       } else if constexpr (kEmu) {
         const uint64_t xs = emu_add(x[u], sigma, flags);
         const uint64_t v = emu_add(xs, sigma ^ kSign, flags);
@@ -623,7 +692,10 @@ OZ_DEVICE int col_slice_planes(const ColSplitParams& P, uint64_t (&x)[16], int c
   }
   uint32_t rest = 0;
 #pragma unroll
-  for (int u = 0; u < 16; ++u) rest |= (uint32_t)x[u] | ((uint32_t)(x[u] >> 32) << 1);
+  for (int u = 0; u < 16; ++u) {
+    const uint64_t r = fx ? (x[u] & kFxRm) : x[u];
+    rest |= (uint32_t)r | ((uint32_t)(r >> 32) << 1);
+  }
   if (rest) z = L + 1;  // still non-zero where a limit check stops the loop
   if (bad & (1u << 16)) flags |= FLAG_NOT_REPRESENTABLE;
   return z;
