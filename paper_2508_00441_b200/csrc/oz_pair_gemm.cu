@@ -36,6 +36,9 @@
 #ifndef OZ_GLB_REG
 #define OZ_GLB_REG 128  // N = 256: Cb columns kept in registers (the rest read-modify-written in C)
 #endif
+#ifndef OZ_REG_INT
+#define OZ_REG_INT 0  // 1: N = 256 grouped kernels add the register half with add_lean too (A/B: 21% slower)
+#endif
 #ifndef OZ_GLB_INT
 #define OZ_GLB_INT 1  // N = 256: C-resident half of Cb added with integer add_lean, before the DFMA half
 #endif
@@ -758,6 +761,7 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
     constexpr bool kTmInt = kEmu || OZ_HW_INT_TMEM;
     constexpr bool kTmFirst = !kEmu && OZ_HW_INT_TMEM;
     constexpr bool kGlbInt = kEmu || OZ_GLB_INT != 0;  // N = 256: C-resident Cb via integer add_lean, first
+    constexpr bool kRegInt = kEmu || (Cfg::kGlbCols > 0 && OZ_REG_INT != 0);  // N = 256: register Cb integer too
     const int quad = warp & 3;               // TMEM lane quadrant this warp may access
     constexpr int kRegHalf = Cfg::kRegHalf;
     const int half = (warp - kLeadWarps) >> 2;        // part: register Cb cols [kRegHalf h, +kRegHalf); TMEM Cb: [kRegCols + kTmHalf*h, +kTmHalf)
@@ -893,7 +897,7 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
 #pragma unroll
             for (int ch = 0; ch < kRegHalf / 16; ++ch) {
               if (ch + 1 < kRegHalf / 16) tmem_ld16(gaddr + half * kRegHalf + (ch + 1) * 16, g[(ch + 1) & 1]);
-              accumulate16<kEmu>(g[ch & 1], ebq + half * kRegHalf + ch * 16, ea_sh, safe, cb + ch * 16, flags);
+              accumulate16<kEmu, kRegInt>(g[ch & 1], ebq + half * kRegHalf + ch * 16, ea_sh, safe, cb + ch * 16, flags);
               if (ch + 1 < kRegHalf / 16) tmem_ld_wait_regs(g[(ch + 1) & 1]);
             }
           }
