@@ -151,6 +151,12 @@ class _FakeCuda:
     def mem_get_info(self):
         return self.free, self.total
 
+    def memory_reserved(self, d=None):  # nothing cached by the allocator
+        return 0
+
+    def memory_allocated(self, d=None):
+        return 0
+
 
 def test_panel_plan_small_problems_unpanelled():
     from paper_2508_00441_b200 import ozgemm
@@ -234,3 +240,23 @@ def test_lp_gemm_refuses_products_whose_accumulation_can_round():
     assert accumulation_is_exact(A, B, f32)
     assert not accumulation_is_exact(A * 1024, B * 1024, get_format("fp16"))
     assert accumulation_is_exact(np.zeros((2, 2)), B[:2], e4m3)
+
+
+def test_panel_plan_counts_cached_allocator_memory():
+    """Blocks torch's caching allocator holds but has not handed out count as
+    free (with them ignored, n = 65536 on one GPU degraded to tiny panels)."""
+    from paper_2508_00441_b200 import ozgemm
+
+    class _Cached(_FakeCuda):
+        def memory_reserved(self, d=None):
+            return 60 << 30
+
+        def memory_allocated(self, d=None):
+            return 0
+
+    ozgemm._TOTAL_MEM.clear()
+    n = 65536
+    bare = ozgemm._panel_plan(n, n, n, 1, type("T", (), {"cuda": _FakeCuda(178, 178 - 96 - 60)}))
+    cached = ozgemm._panel_plan(n, n, n, 1, type("T", (), {"cuda": _Cached(178, 178 - 96 - 60)}))
+    assert cached[0] * cached[1] > bare[0] * bare[1]
+    assert cached == ozgemm._panel_plan(n, n, n, 1, type("T", (), {"cuda": _FakeCuda(178, 178 - 96)}))
