@@ -33,18 +33,6 @@
 #ifndef OZ_TERM_FMA
 #define OZ_TERM_FMA 1  // HW-mode safe terms: DFMA(double(G), 2^(eA+eB), Cb) instead of bit assembly + DADD
 #endif
-#ifndef OZ_GLB_REG
-#define OZ_GLB_REG 128  // N = 256: Cb columns kept in registers (the rest read-modify-written in C)
-#endif
-#ifndef OZ_REG_INT
-#define OZ_REG_INT 0  // 1: N = 256 grouped kernels add the register half with add_lean too (A/B: 21% slower)
-#endif
-#ifndef OZ_GLB_INT
-#define OZ_GLB_INT 1  // N = 256: C-resident half of Cb added with integer add_lean, before the DFMA half
-#endif
-#ifndef OZ_HW_INT_TMEM
-#define OZ_HW_INT_TMEM 0  // 1: hardware mode adds the TMEM third of Cb with integer add_lean, first (A/B: slower)
-#endif
 #ifndef OZ_DIAGNOSTICS
 #define OZ_DIAGNOSTICS 0  // 1: per-pair clock trace + OZ_DEBUG_MODE hooks (tools/ only; never the product)
 #endif
@@ -82,7 +70,7 @@ struct PairCfg {
   static constexpr int kBRows = kN / kCta;                    // B rows staged per CTA
   static constexpr int kStageBytes = (kPM + kBRows) * 128;    // per CTA
   static constexpr int kRegCols =
-      kEmu ? 0 : (kN == 256 ? OZ_GLB_REG : (kEpi == 12 ? kN * 3 / 4 : (kN < 128 ? kN : 128)));  // Cb cols in registers
+      kEmu ? 0 : (kN == 256 ? 128 : (kEpi == 12 ? kN * 3 / 4 : (kN < 128 ? kN : 128)));  // Cb cols in registers
   static constexpr int kRegHalf = kRegCols / kParts;          // ... per epilogue thread
   static constexpr int kAccBufs = kN == 64 ? 4 : ((kEmu || kN != 128) ? 2 : 4);
   // N = 256 (fixed-step grouped mode, single k-block): both accumulators fill TMEM,
@@ -756,12 +744,15 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
     constexpr int kRegCols = Cfg::kRegCols;
     constexpr int kTmHalf = Cfg::kTmCols / Cfg::kParts;  // TMEM-resident Cb columns per thread
     constexpr int kGlbHalf = Cfg::kGlbCols / Cfg::kParts;  // C-resident Cb columns per thread (N = 256)
-    // TMEM-resident Cb with integer adds (always in emulated mode; hardware mode:
-    // OZ_HW_INT_TMEM), processed before the register part.
-    constexpr bool kTmInt = kEmu || OZ_HW_INT_TMEM;
-    constexpr bool kTmFirst = !kEmu && OZ_HW_INT_TMEM;
-    constexpr bool kGlbInt = kEmu || OZ_GLB_INT != 0;  // N = 256: C-resident Cb via integer add_lean, first
-    constexpr bool kRegInt = kEmu || (Cfg::kGlbCols > 0 && OZ_REG_INT != 0);  // N = 256: register Cb integer too
+    // Integer adds (add_lean; bit-identical to the DADD/DFMA path): everything in
+    // emulated mode; in hardware mode the C-resident half of Cb of the 256-column
+    // grouped kernel, issued before the register half's DFMAs (integer work is not
+    // held back by the MMAs).  Measured and dropped (profiles/): integer adds for
+    // hardware mode's TMEM third (hw_int_tmem_ab_r02.txt), for the register half
+    // and all of Cb in C at N = 256 (wide_tiles_ab_r02.txt).
+    constexpr bool kTmInt = kEmu;
+    constexpr bool kGlbInt = true;
+    constexpr bool kRegInt = kEmu;
     const int quad = warp & 3;               // TMEM lane quadrant this warp may access
     constexpr int kRegHalf = Cfg::kRegHalf;
     const int half = (warp - kLeadWarps) >> 2;        // part: register Cb cols [kRegHalf h, +kRegHalf); TMEM Cb: [kRegCols + kTmHalf*h, +kTmHalf)
@@ -840,7 +831,7 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
                             (kEmu || !OZ_TERM_FMA || (ea + 1023 + mm.x >= 1 && ea + 1023 + mm.y <= 2046));
           const uint32_t gaddr = tmem + lane_base + buf * kN;
           auto tmem_part = [&]() {
-            // Integer adds (kTmInt): rolled, so the code stays in the instruction cache.
+            // Integer adds (emulated mode): rolled, so the code stays in the instruction cache.
 #pragma unroll(kTmInt || kTmHalf < 16 ? 1 : kTmHalf / 16)
             for (int ch = 0; ch < kTmHalf / 16; ++ch) {
               uint32_t g[16], w[32];
@@ -866,9 +857,8 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
           };
           auto glb_part = [&]() {
             // C-resident part (N = 256, first k-block only): Cb = C[row, cols] (+0
-            // before this tile's first group), Cb += T, C[row, cols] = Cb.  OZ_GLB_INT:
-            // integer add_lean (issued before the register part's DFMAs, so it is not
-            // held back behind them; bit-identical).
+            // before this tile's first group), Cb += T, C[row, cols] = Cb, with the
+            // integer add_lean.
             const int col0 = tn * kN + kRegCols + half * kGlbHalf;
 #pragma unroll(kGlbInt || kGlbHalf < 16 ? 1 : kGlbHalf / 16)
             for (int ch = 0; ch < kGlbHalf / 16; ++ch) {
@@ -883,10 +873,7 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
             }
             glb_init = true;
           };
-          if constexpr (kGlbHalf > 0 && kGlbInt) glb_part();
-          // Hardware mode, integer TMEM part: issued first, while the tensor pipe runs
-          // (integer ops are not held back by the MMAs; the register part's DFMAs are).
-          if constexpr (kTmHalf > 0 && kTmFirst) tmem_part();
+          if constexpr (kGlbHalf > 0) glb_part();
 
           // Software-pipelined TMEM reads: chunk ch+1 loads while chunk ch is
           // accumulated (the wait names the registers so no use is hoisted above it).
@@ -902,8 +889,7 @@ __global__ void __launch_bounds__(32 * kLeadWarps + 32 * kEpi, 1)
             }
           }
           if (tr) P.trace[acc_it * 8 + 7] = clock64();
-          if constexpr (kTmHalf > 0 && !kTmFirst) tmem_part();
-          if constexpr (kGlbHalf > 0 && !kGlbInt) glb_part();
+          if constexpr (kTmHalf > 0) tmem_part();
         }
         tc_fence_before();
         __syncwarp();

@@ -490,3 +490,29 @@ def test_fixed_step_wide_tiles_bitwise(cuda, shape, pair_variant):
         Cref, _ = oracle.oz_gemm_fixed(A, B, "fp8e4m3", "fp32", 0, None, "smallest-first", cut)
         nbad = int(np.sum(bits(res.C) != bits(Cref)))
         assert nbad == 0, f"cut {cut}: {nbad}/{m * n} entries differ"
+
+
+@pytest.mark.parametrize("kw", [{}, {"pair_cutoff": 9, "slice_exponents": "fixed"}, {"fp64_emulation": True}],
+                         ids=["defaults", "fixed9", "emu"])
+def test_tuning_knobs_keep_bits(cuda, kw):
+    """oz_set_epilogue_warps(12) (N = 192 kernel) and oz_set_pair_schedule(1)
+    (exclusive epilogue windows) change scheduling only: C is bitwise the
+    default over several tile waves."""
+    from paper_2508_00441_b200 import _lib
+
+    torch = cuda
+    oz = _oz()
+    rng = np.random.default_rng(8)
+    A = torch.from_numpy(spread_matrix(rng, 1500, 1024, 1.0)).cuda()
+    B = torch.from_numpy(spread_matrix(rng, 1024, 2100, 1.0)).cuda()
+    cfg = oz.GemmConfig(oz.get_format("fp8e4m3"), oz.get_format("fp32"), **kw)
+    ref, _ = oz.oz_gemm_device(A, B, cfg)
+    try:
+        for warps, sched in ((12, 0), (8, 1), (12, 1)):
+            _lib.call("oz_set_epilogue_warps", warps)
+            _lib.call("oz_set_pair_schedule", sched)
+            C, _ = oz.oz_gemm_device(A, B, cfg)
+            assert torch.equal(C.view(torch.int64), ref.view(torch.int64)), (warps, sched)
+    finally:
+        _lib.call("oz_set_epilogue_warps", 8)
+        _lib.call("oz_set_pair_schedule", 0)
