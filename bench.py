@@ -365,19 +365,25 @@ def main():
     mma_flops = 2.0 * n * n * n * pairs_exec
     gemm_ms = statistics.mean(gemm_s) * 1e3
     peaks = measured_peaks()
-    fp8_peak = 2.0 * peaks["bf16"]
+    # K3 is timed inside back-to-back steps (~0.1 s each, power-capped), so the
+    # roofline is the SUSTAINED dense rate (MEASURED_PEAKS.json, bf16 back to
+    # back for 4 s, x2 for FP8); the burst-peak fraction is reported beside it.
+    fp8_peak = 2.0 * (peaks["bf16_sustained"] or peaks["bf16"])
+    fp8_burst = 2.0 * peaks["bf16"]
     achieved = mma_flops / (gemm_ms / 1e3) / 1e12
     traffic = None
     prof = ROOT / "profiles" / "pair_gemm_r02_defaults_final_summary.json"
     if prof.exists() and args.n == 8192 and args.pair_cutoff is None and args.type2 == "fp8e4m3" and not args.kblock:
         traffic = json.loads(prof.read_text())["traffic_bytes_per_launch"]  # ncu --set full, same workload
     roofline = {"bound": "tensor", "achieved": achieved, "peak": fp8_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp8_peak, "traffic": traffic,
+                "frac": achieved / fp8_peak, "peak_burst": fp8_burst, "frac_burst": achieved / fp8_burst,
+                "traffic": traffic,
                 "traffic_source": "dram read+write per launch, ncu --set full of this workload, "
                                   "profiles/pair_gemm_r02_defaults_final_summary.json"
                 if traffic else None,
                 "kernel": "pair_gemm_kernel<false> (fused slice-pair GEMM + FP64 accumulation)",
-                "peak_source": f"dense fp8 = 2 x measured dense bf16 ({peaks['source']})",
+                "peak_source": f"dense fp8 = 2 x measured sustained dense bf16 ({peaks['source']}); "
+                               f"peak_burst = 2 x the burst figure",
                 "algorithmic_flops_per_launch": mma_flops,
                 "pairs_per_tile_executed_mean": pairs_exec, "pairs_reference": blk.gemms,
                 "kernel_ms": gemm_ms, "split_ms": statistics.mean(slice_s) * 1e3}
@@ -508,12 +514,14 @@ def run_strong(args):
     gemm_ms = statistics.mean(gemm_s) * 1e3
     tile_mma = 2.0 * (r1 - r0) * (c1 - c0) * n * blk.gemms
     peaks = measured_peaks()
-    fp8_peak = 2.0 * peaks["bf16"]
+    fp8_peak = 2.0 * (peaks["bf16_sustained"] or peaks["bf16"])  # seconds-long run: sustained rate
+    fp8_burst = 2.0 * peaks["bf16"]
     achieved = tile_mma / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     roofline = {"bound": "tensor", "achieved": achieved, "peak": fp8_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp8_peak if achieved else None, "traffic": None,
+                "frac": achieved / fp8_peak if achieved else None, "peak_burst": fp8_burst,
+                "frac_burst": achieved / fp8_burst if achieved else None, "traffic": None,
                 "kernel": "pair_gemm_kernel (this rank's C tile; all of its panel passes)",
-                "peak_source": f"dense fp8 = 2 x measured dense bf16 ({peaks['source']})",
+                "peak_source": f"dense fp8 = 2 x measured sustained dense bf16 ({peaks['source']})",
                 "algorithmic_flops_per_launch": tile_mma, "kernel_ms": gemm_ms,
                 "split_ms": statistics.mean(slice_s) * 1e3}
     # Bitwise parity sample of this rank's tile (rank 0): the oracle on a few
