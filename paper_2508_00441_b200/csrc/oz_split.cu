@@ -226,6 +226,17 @@ OZ_DEVICE uint64_t fx_slice(uint64_t st, int dg, int& k) {
   return rm2 == 0 ? (st & ~((1ull << 54) - 1)) : (rm2 | ((uint64_t)sg2 << 53) | (st & ~((1ull << 54) - 1)));
 }
 
+// Row-max key of a fixed-point residual, ordered like elem_key for what col_c0
+// reads (exponent field in bits 21+, non-zero low bits iff |r| is not a power of
+// two): |r| = rm * 2^(g0 - sh0) (sh0 unclamped), normal for rows without tiny inputs.
+OZ_DEVICE uint32_t fx_key(uint64_t st, int g0) {
+  const uint64_t rm = st & kFxRm;
+  if (rm == 0) return 0u;
+  const int pos = 63 - __clzll((long long)rm);
+  const int ef = pos + g0 - (int)(st >> 54) + 1023;
+  return ((uint32_t)ef << 21) | ((rm & (rm - 1)) != 0 ? 1u : 0u);
+}
+
 
 
 // One reference iteration over this thread's elements (slicing.py:162-176):
@@ -234,12 +245,12 @@ OZ_DEVICE uint64_t fx_slice(uint64_t st, int dg, int& k) {
 // rows holding inputs below 2^-969, or code tables with unrepresentable entries).
 // kKey = false (fixed-step fast path, kWrite only): return the OR of the codes
 // instead of the max key (the row max is not needed there).
-// kFx (emulated fixed-step fast path): x[] holds fx_state() words and g is the
-// plane's grid offset dg = g_p - g_0.
+// kFx (emulated fixed-point paths): x[] holds fx_state() words and g is the
+// plane's grid offset dg = g_p - g_0; with kKey the max key is fx_key(., g0).
 template <int kThreads, int kEPT, int kEB, bool kEmu, bool kWrite, bool kChecked, bool kKey = true, bool kFx = false>
 OZ_DEVICE uint32_t slice_iteration(uint64_t (&x)[kEPT], const uint64_t sigma, const int g, const uint32_t* __restrict__ tblc,
                                    int K, uint8_t* plane, int64_t base, int t, int64_t ld, uint32_t& flags,
-                                   uint32_t& bad, const int pack6) {
+                                   uint32_t& bad, const int pack6, const int g0 = 0) {
   constexpr int kV = 16 / kEB;
   constexpr int kChunks = kEPT / kV;
   uint32_t key = 0;
@@ -272,7 +283,8 @@ OZ_DEVICE uint32_t slice_iteration(uint64_t (&x)[kEPT], const uint64_t sigma, co
         if constexpr (kChecked) bad |= ent;
         codes[u] = ent;
       }
-      if constexpr (kKey) key = max(key, elem_key(xn));
+      if constexpr (kKey && kFx) key = max(key, fx_key(xn, g0));
+      else if constexpr (kKey) key = max(key, elem_key(xn));
       else key |= codes[u];
       if constexpr (kChecked) {
         const uint32_t ef = (uint32_t)((xn >> 52) & 0x7FF);
@@ -316,8 +328,11 @@ OZ_DEVICE uint32_t slice_iteration(uint64_t (&x)[kEPT], const uint64_t sigma, co
   return key;
 }
 
+// Two CTAs per SM when a CTA holds <= 8192 elements (64 registers per thread at 512
+// threads; one resident CTA with the full register file measured slower for the
+// emulated kernels too: 4.7 vs 3.4 ms adaptive, 2.25 vs 2.03 ms fixed-step per
+// 8192^2 operand, profiles/split_emu_r02.txt).
 template <int kThreads, int kEPT, int kCL, int kEB, bool kEmu>
-// Two CTAs per SM when a CTA holds <= 8192 elements (64 registers per thread at 512 threads).
 __global__ void __launch_bounds__(kThreads, kThreads * kEPT <= 8192 ? 2 : 1) split_fused_kernel(const FusedSplitParams P) {
   constexpr int kV = 16 / kEB;          // elements per 16-byte plane store
   constexpr int kChunks = kEPT / kV;
@@ -472,7 +487,13 @@ __global__ void __launch_bounds__(kThreads, kThreads * kEPT <= 8192 ? 2 : 1) spl
       if (write && t == 0 && rank == 0)
         for (int p = 0; p < cnt; ++p) P.expo[(int64_t)p * P.rows + row] = c0 - p * P.fixed_w;
     }
-  } else
+  } else {
+  // Emulated mode, rows without tiny inputs: this thread's residuals in fixed point
+  // (fx_state / fx_slice, as in the fixed-step path) once c_0 is known — the
+  // grid offset of slice p is dg = c_p - c_0 — unless an element is so far below
+  // the row max that its shift would exceed fx_state's 10-bit field.
+  bool fxa = false;
+  int c0 = 0;
   for (int it = 0;; ++it) {
     const uint32_t m = row_max(key, it);
     if (m == 0) break;
@@ -496,6 +517,29 @@ __global__ void __launch_bounds__(kThreads, kThreads * kEPT <= 8192 ? 2 : 1) spl
     }
     const uint64_t sigma = ((uint64_t)sig_exp << 52) | (1ull << 51);
     uint8_t* plane = row_plane0 + (int64_t)it * plane_stride;
+    if constexpr (kEmu) {
+      if (it == 0 && write && !checked) {
+        c0 = c;
+        const int g0 = c + P.rho - 53;
+        fxa = true;
+#pragma unroll
+        for (int i = 0; i < kEPT; ++i)
+          if ((x[i] << 1) != 0 && g0 - (int)((x[i] >> 52) & 0x7FF) + 1075 > 1000) fxa = false;
+        if (fxa) {
+#pragma unroll
+          for (int i = 0; i < kEPT; ++i) x[i] = fx_state(x[i], g0);
+        }
+      }
+      if (fxa) {
+        // |dg| stays far below the field's headroom: planes <= cap, and every
+        // jump c_p -> c_(p+1) below c_p - w skips only all-zero digit positions.
+        key = slice_iteration<kThreads, kEPT, kEB, kEmu, true, false, true, true>(
+            x, sigma, c - c0, tblc, K, plane, base, t, P.ld, flags, bad, P.pack6, c0 + P.rho - 53);
+        if (write && t == 0 && rank == 0) P.expo[(int64_t)it * P.rows + row] = c;
+        ++cnt;
+        continue;
+      }
+    }
     if (!write)
       key = slice_iteration<kThreads, kEPT, kEB, kEmu, false, true>(x, sigma, c + P.rho - 53, tblc, K, plane, base, t, P.ld,
                                                                     flags, bad, P.pack6);
@@ -507,6 +551,7 @@ __global__ void __launch_bounds__(kThreads, kThreads * kEPT <= 8192 ? 2 : 1) spl
                                                                     flags, bad, P.pack6);
     if (write && t == 0 && rank == 0) P.expo[(int64_t)it * P.rows + row] = c;
     ++cnt;
+  }
   }
   if (bad & (1u << 16)) flags |= FLAG_NOT_REPRESENTABLE;
   if (t == 0 && rank == 0) {

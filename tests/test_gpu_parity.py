@@ -516,3 +516,88 @@ def test_tuning_knobs_keep_bits(cuda, kw):
     finally:
         _lib.call("oz_set_epilogue_warps", 8)
         _lib.call("oz_set_pair_schedule", 0)
+
+
+def _structured_rows(rng, rows, kb):
+    """Rows that defeat the adaptive split's exponent speculation (a residual max
+    below a quarter of the grid step, early ends, single elements) mixed with
+    random rows."""
+    X = spread_matrix(rng, rows, kb, 1.0)
+    X[0] = 1.0                                   # ends after one slice
+    X[1] = 1.0 + 2.0 ** -30                      # residual 2^-30: mismatch at slice 1
+    X[2] = 0.0
+    X[2, kb // 2] = -3.0 + 2.0 ** -40            # single element
+    X[3] = rng.integers(-7, 8, kb).astype(np.float64) * (1.0 + 2.0 ** -22 + 2.0 ** -47)
+    X[4] = np.ldexp(1.0, rng.integers(-20, 20, kb))  # powers of two over a range
+    X[5] = (1.0 + 2.0 ** -20 + 2.0 ** -45) * np.sign(rng.standard_normal(kb))
+    X[6, ::3] = 2.0 ** -35                       # small entries next to random ones
+    X[7] = np.where(rng.random(kb) < 0.01, rng.standard_normal(kb), 0.0)  # sparse
+    return X
+
+
+@pytest.mark.parametrize("fmt", ["fp8e4m3", "fp16", "bf16"])
+@pytest.mark.parametrize("emu", [False, True])
+@pytest.mark.parametrize("kb", [37, 4096, 8192, 20000])
+def test_split_speculation_structured_rows(cuda, fmt, emu, kb):
+    """The batched adaptive split (speculated exponents, one reduction per batch,
+    replay on a mismatch) gives the reference's slices, exponents and counts."""
+    import oracle
+
+    oz = _oz()
+    rng = np.random.default_rng(kb + 7 * emu)
+    X = _structured_rows(rng, 12, kb)
+    params = oz.compute_params(53, oz.get_format(fmt).mant_bits, 24, kb)
+    ss = oz.slice_matrix(X, "rows", oz.get_format(fmt), params, "emu" if emu else "fp64")
+    coeff, expo, cnt, s, flags = oracle.split_rows(X, params.rho, emu)
+    assert flags == 0 and ss.s == s
+    for p in range(s):
+        assert np.array_equal(bits(ss.coeff[p]), bits(coeff[p])), f"coeff plane {p}"
+        assert np.array_equal(ss.expo[p], expo[p].astype(np.int64)), f"expo plane {p}"
+
+
+@pytest.mark.parametrize("emu", [False, True])
+def test_oz_gemm_structured_rows_bitwise(cuda, emu):
+    import oracle
+
+    oz = _oz()
+    rng = np.random.default_rng(99)
+    A = _structured_rows(rng, 130, 700)
+    B = _structured_rows(rng, 140, 700).T.copy()
+    cfg = oz.GemmConfig(oz.get_format("fp8e4m3"), oz.get_format("fp32"), fp64_emulation=emu)
+    C = oz.oz_gemm(A, B, cfg).C
+    Cref, _ = oracle.oz_gemm(A, B, "fp8e4m3", "fp32", 0, emu)
+    assert np.array_equal(bits(C), bits(Cref))
+
+
+
+
+
+@pytest.mark.parametrize("fixed", [False, True])
+def test_emulated_split_fixed_point_rows(cuda, fixed):
+    """Emulated row split at kb = 8192 (fixed-point residuals: fx_state/fx_slice,
+    keys from fx_key), adaptive and fixed-step: slices, exponents and counts are
+    the oracle's, incl. structured rows and a row whose elements span too many
+    binades for the fixed-point shift field (that thread keeps FP64 words)."""
+    import oracle
+
+    torch = cuda
+    oz = _oz()
+    rng = np.random.default_rng(5 + fixed)
+    X = _structured_rows(rng, 40, 8192)
+    X[20, 5] = 2.0 ** 400
+    X[20, 6] = 2.0 ** -600
+    f = oz.get_format("fp8e4m3")
+    params = oz.compute_params(53, f.mant_bits, 24, 8192)
+    if fixed:
+        ds, _, flags, _ = _fixed_split_pair(torch, X, "fp8e4m3", True, 12, False)
+        coeff, expo, cnt, s = oracle.split_rows_fixed(X, params.rho, 12)
+        assert flags == 0 and ds.s == s
+        assert np.array_equal(ds.row_cnt.cpu().numpy(), cnt)
+        ss = oz.slicing.device_to_sliceset(ds, "rows", params)
+    else:
+        ss = oz.slice_matrix(X, "rows", f, params, "emu")
+        coeff, expo, _, s, flags = oracle.split_rows(X, params.rho, True)
+        assert flags == 0 and ss.s == s
+    for p in range(s):
+        assert np.array_equal(bits(ss.coeff[p]), bits(coeff[p])), f"coeff plane {p}"
+        assert np.array_equal(np.asarray(ss.expo[p]), np.asarray(expo[p]).astype(np.int64)), f"expo plane {p}"
