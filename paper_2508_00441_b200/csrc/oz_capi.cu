@@ -225,7 +225,10 @@ int launch_fused_cfg(const oz::FusedSplitParams& P, cudaStream_t st) {
   if (need <= 4096) return launch_fused<256, 16, 1, kEB, kEmu>(P, st);
   // Fixed-step fast path (no per-slice reductions): 16 elements per thread and
   // 2 x 16 warps per SM hide the FP64 latency better than 32 elements x 16 warps.
-  if (need <= 8192 && P.fixed_w > 0 && P.max_planes > 0) return launch_fused<512, 16, 1, kEB, kEmu>(P, st);
+  // The emulated (integer) adaptive split gains from the 32 warps too (3.43 ->
+  // 3.06 ms per 8192^2 operand); the hardware one does not (0.79 -> 0.84 ms,
+  // profiles/split_emu_r02.txt).
+  if (need <= 8192 && (kEmu || (P.fixed_w > 0 && P.max_planes > 0))) return launch_fused<512, 16, 1, kEB, kEmu>(P, st);
   if (need <= 8192) return launch_fused<256, 32, 1, kEB, kEmu>(P, st);
   if (need <= 16384) return launch_fused<512, 32, 1, kEB, kEmu>(P, st);
   if (need <= 32768) return launch_fused<256, 32, 4, kEB, kEmu>(P, st);
