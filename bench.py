@@ -443,7 +443,7 @@ def run_strong(args):
     import torch.distributed as dist
 
     import paper_2508_00441_b200 as oz
-    from paper_2508_00441_b200.distributed import TileGrid
+    from paper_2508_00441_b200.distributed import TileGrid, oz_gemm_tile
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -482,7 +482,7 @@ def run_strong(args):
             grid.distribute_panels(dist, groups, rank, A, B)
         if timing:
             ev_d[1].record()
-        _, st = oz.oz_gemm_device(A, B, cfg, out=C, graph=not args.no_graph)
+        _, st = oz_gemm_tile(A, B, cfg, out=C, graph=not args.no_graph)
         return st
 
     for _ in range(args.warmup):

@@ -86,8 +86,12 @@ class TileGrid:
         return split_extent(m, self.rows, i), split_extent(n, self.cols, j)
 
 
-def oz_gemm_tile(A_panel, B_panel, cfg, out=None):
-    """This rank's C tile from its panels with the single-GPU fused kernels."""
+def oz_gemm_tile(A_panel, B_panel, cfg, out=None, graph: bool = False):
+    """This rank's C tile C[I, J] = A_I @ B_J from its (distributed) panels with
+    the single-GPU fused kernels — no reduction: slicing is row/column-local and
+    the pair order is per element, so the tile is bitwise the single-GPU C's
+    block.  Returns (C_tile, OzStats); used by bench.py's config-5 mode and the
+    multi-rank GPU tests."""
     from .ozgemm import oz_gemm_device
 
-    return oz_gemm_device(A_panel, B_panel, cfg, out=out)
+    return oz_gemm_device(A_panel, B_panel, cfg, out=out, graph=graph)

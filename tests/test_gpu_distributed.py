@@ -40,7 +40,7 @@ def _worker(rank, world, port, m, n, k, cfg_kw, out_dir):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_2508_00441_b200 as oz
-    from paper_2508_00441_b200.distributed import TileGrid
+    from paper_2508_00441_b200.distributed import TileGrid, oz_gemm_tile
 
     grid = TileGrid.for_world(world)
     groups = grid.make_groups(dist)
@@ -54,7 +54,7 @@ def _worker(rank, world, port, m, n, k, cfg_kw, out_dir):
         Bp.copy_(torch.from_numpy(np.ascontiguousarray(B[:, c0:c1])))
     grid.distribute_panels(dist, groups, rank, Ap, Bp)
     cfg = oz.GemmConfig(oz.get_format("fp8e4m3"), oz.get_format("fp32"), **cfg_kw)
-    C, _ = oz.oz_gemm_device(Ap, Bp, cfg)
+    C, _ = oz_gemm_tile(Ap, Bp, cfg)
     np.save(os.path.join(out_dir, f"tile{rank}.npy"), C.cpu().numpy())
     dist.barrier()
     dist.destroy_process_group()
