@@ -220,8 +220,10 @@ int oz_dd_gemm(const double* A, const double* B, double* C, int64_t m, int64_t n
 /* out[i] = a[i] + b[i] on FP64 bit patterns with the integer-only emulation:
  * mode 0 = emu_add (restates fp64emu._add_core, fp64emu.py:193-251; range errors
  * set OZ_FLAG_EMU_RANGE), mode 1 = the epilogue's fast_add, mode 2 = the
- * emulated epilogue's add_lean (same results).
- * Backs the CLI's `verify --suite fp64emu` (cli.py:190-222). */
+ * emulated epilogue's add_lean (same results); mode 3: out = a * b, integer-only
+ * (fp64emu._mul_core, fp64emu.py:150-187); mode 4: out = (a < b) ? 1 : 0
+ * (fp64emu._lt_core, :257-266).
+ * Backs the CLI's `verify --suite fp64emu` (cli.py:177-200). */
 int oz_emu_add_batch(const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t n, int mode, uint32_t* flags,
                      void* stream);
 

@@ -315,10 +315,51 @@ PairPlan plan_pair(int64_t m, int64_t n, int64_t kb, int elem_bytes, int sx, int
   return pl;
 }
 
+// Integer-only FP64 multiply (restates fp64emu._mul_core, fp64emu.py:150-187): normal or
+// zero operands (others, and results outside the normal range, set FLAG_EMU_RANGE as the
+// reference raises RangeError); 53 x 53-bit significand product, RNE to 53 bits.
+__device__ uint64_t emu_mul(uint64_t a, uint64_t b, uint32_t& f) {
+  constexpr uint64_t kSgn = 1ull << 63, kFrac = (1ull << 52) - 1;
+  const uint32_t ea = (uint32_t)(a >> 52) & 0x7FFu, eb = (uint32_t)(b >> 52) & 0x7FFu;
+  if ((ea == 0 && (a & kFrac)) || ea == 0x7FFu || (eb == 0 && (b & kFrac)) || eb == 0x7FFu) f |= oz::FLAG_EMU_RANGE;
+  const uint64_t sign = (a ^ b) & kSgn;
+  if ((a & ~kSgn) == 0 || (b & ~kSgn) == 0) return sign;  // a zero factor: signed zero
+  const uint64_t ma = (a & kFrac) | (1ull << 52), mb = (b & kFrac) | (1ull << 52);
+  const uint64_t lo = ma * mb, hi = __umul64hi(ma, mb);  // product in [2^104, 2^106)
+  const int t = (int)((hi >> 41) & 1u);
+  const int sh = 52 + t;
+  uint64_t sig = (hi << (64 - sh)) | (lo >> sh);
+  const uint64_t rem = lo & ((1ull << sh) - 1), half = 1ull << (sh - 1);
+  sig += (rem > half || (rem == half && (sig & 1u))) ? 1u : 0u;  // guard && (sticky || odd)
+  const int carry = sig == (1ull << 53) ? 1 : 0;
+  sig >>= carry;
+  const int e = (int)ea + (int)eb - 1023 + t + carry;
+  if (e < 1 || e > 2046) {
+    f |= oz::FLAG_EMU_RANGE;
+    return sign;
+  }
+  return sign | ((uint64_t)e << 52) | (sig & kFrac);
+}
+
+// fp64emu._lt_core (fp64emu.py:257-266): -0 == +0, sign-magnitude -> monotone key.
+__device__ uint64_t emu_order_key(uint64_t x) {
+  constexpr uint64_t kSgn = 1ull << 63;
+  const uint64_t v = (x & ~kSgn) == 0 ? 0ull : x;
+  return (v & kSgn) ? ~v : (v | kSgn);
+}
+
 __global__ void emu_add_batch_kernel(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
                                      uint64_t* __restrict__ out, int64_t n, int mode, uint32_t* flags) {
   uint32_t f = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (mode == 3) {
+      out[i] = emu_mul(a[i], b[i], f);
+      continue;
+    }
+    if (mode == 4) {
+      out[i] = emu_order_key(a[i]) < emu_order_key(b[i]) ? 1ull : 0ull;
+      continue;
+    }
     if (mode == 2) {  // add_lean on its domain (normal or zero operands), emu_add otherwise / when slow
       const uint32_t ea = (uint32_t)(a[i] >> 52) & 0x7FFu, eb = (uint32_t)(b[i] >> 52) & 0x7FFu;
       const bool dom = (ea != 0 || (a[i] << 1) == 0) && (eb != 0 || (b[i] << 1) == 0) && ea != 0x7FFu && eb != 0x7FFu;
@@ -724,7 +765,7 @@ int oz_pair_gemm_grouped(const void* a_planes, const void* b_planes, int64_t ld_
 
 int oz_emu_add_batch(const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t n, int mode, uint32_t* flags,
                      void* stream) {
-  if (n < 0 || mode < 0 || mode > 2) return OZ_EINVAL;
+  if (n < 0 || mode < 0 || mode > 4) return OZ_EINVAL;
   if (n == 0) return OZ_OK;
   if (!a || !b || !out || !flags) return OZ_EINVAL;
   const int64_t blocks = (n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096;

@@ -80,3 +80,4 @@ def test_accuracy_and_verify(cuda, capsys):
     assert code == 0 and rep["pass"] is True
     assert set(rep["suites"]) == {"fp64emu", "reconstruction", "errorfree"}
     assert all(s["checks"] > 0 and s["failures"] == 0 for s in rep["suites"].values())
+    assert rep["suites"]["fp64emu"]["checks"] == 3 * 2000 + 1000  # reference schema: add, sub, mul + lt

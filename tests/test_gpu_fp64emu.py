@@ -62,3 +62,37 @@ def test_device_integer_adds_match_ieee(cuda, mode):
         assert bad.size == 0, (mode, [(hex(int(a[i])), hex(int(b[i])), hex(int(got[i])), hex(int(want[i])))
                                       for i in bad[:4]])
         assert fl == 0
+
+
+def test_device_mul_and_lt(cuda):
+    """oz_emu_add_batch modes 3 / 4: integer-only multiply (fp64emu._mul_core,
+    RNE incl. the carry into the next binade and exact ties) and the order
+    compare (_lt_core: -0 == +0) against IEEE; range errors flagged."""
+    torch = cuda
+    rng = np.random.default_rng(11)
+    n = 1 << 18
+    sig = rng.integers(0, 1 << 52, size=(2, n), dtype=np.int64).astype(np.uint64)
+    e = rng.integers(600, 1450, size=(2, n)).astype(np.uint64)
+    s = rng.integers(0, 2, size=(2, n)).astype(np.uint64) << np.uint64(63)
+    ab = (e << np.uint64(52)) | sig | s
+    # significands that multiply to exact ties / all-ones carries
+    ab[0, :1000] = (ab[0, :1000] & ~np.uint64((1 << 52) - 1)) | np.uint64((1 << 52) - 1)
+    ab[1, :1000] = (ab[1, :1000] & ~np.uint64((1 << 52) - 1)) | np.uint64((1 << 52) - 1)
+    ab[0, 1000:2000] = (ab[0, 1000:2000] & ~np.uint64((1 << 52) - 1)) | np.uint64(1 << 51)  # 1.5
+    ab[1, 1000:2000] = (ab[1, 1000:2000] & ~np.uint64((1 << 52) - 1)) | np.uint64(1)        # 1 + ulp
+    ab[0, 2000:2100] = np.uint64(0)
+    ab[1, 2100:2200] = np.uint64(1 << 63)                                                     # -0
+    a, b = ab[0].view(np.float64), ab[1].view(np.float64)
+    got, fl = _run(torch, a, b, 3)
+    assert fl == 0
+    assert np.array_equal(got, (a * b).view(np.uint64))
+    got, fl = _run(torch, a, b, 4)
+    assert np.array_equal(got.astype(bool), a < b)
+    # -0 < +0 is false both ways; equal operands are not less
+    z = np.array([0.0, -0.0, 1.5], dtype=np.float64)
+    got, _ = _run(torch, z, np.array([-0.0, 0.0, 1.5]), 4)
+    assert not got.any()
+    # out of the normal range: flagged (the reference raises RangeError)
+    big = np.array([2.0 ** 600, 2.0 ** -600], dtype=np.float64)
+    _, fl = _run(torch, big, big, 3)
+    assert fl != 0
