@@ -601,3 +601,66 @@ def test_emulated_split_fixed_point_rows(cuda, fixed):
     for p in range(s):
         assert np.array_equal(bits(ss.coeff[p]), bits(coeff[p])), f"coeff plane {p}"
         assert np.array_equal(np.asarray(ss.expo[p]), np.asarray(expo[p]).astype(np.int64)), f"expo plane {p}"
+
+
+@pytest.mark.parametrize("t2,kbk", [("fp8e4m3", 0), ("fp8e5m2", 0), ("bf16", 256), ("fp6e3m2", 0)])
+def test_type3_fp64_within_exact_range(cuda, t2, kbk):
+    """type3 = fp64 (the reference accumulates lp_gemm in FP64, per-step RNE):
+    wherever every partial sum of a k-block fits the FP32 tensor-core
+    accumulator exactly (kb <= 2^(24 - 2 (53 - rho))), both accumulations are
+    exact, so C is the reference's bit for bit."""
+    import oracle
+
+    oz = _oz()
+    rng = np.random.default_rng(64)
+    A = spread_matrix(rng, 150, 600, 1.0)
+    B = spread_matrix(rng, 600, 130, 1.0)
+    cfg = oz.GemmConfig(oz.get_format(t2), oz.get_format("fp64"), k_block=kbk)
+    res = oz.oz_gemm(A, B, cfg)
+    Cref, info = oracle.oz_gemm(A, B, t2, "fp64", kbk, False)
+    assert info["flags"] == 0
+    assert [(b.k_lo, b.k_hi, b.s_x, b.s_y) for b in res.stats.blocks] == info["blocks"]
+    assert np.array_equal(bits(res.C), bits(Cref))
+
+
+def test_type3_fp64_beyond_exact_range_raises(cuda):
+    """FP16 slices with type3 = fp64 get rho = 42 (11-bit digits): a k-block of
+    600 would need 35-bit partial sums — not available on the tensor cores, so
+    the call raises instead of returning a differently rounded C."""
+    oz = _oz()
+    rng = np.random.default_rng(65)
+    A = spread_matrix(rng, 64, 600, 1.0)
+    B = spread_matrix(rng, 600, 64, 1.0)
+    with pytest.raises(NotImplementedError):
+        oz.oz_gemm(A, B, oz.GemmConfig(oz.get_format("fp16"), oz.get_format("fp64")))
+
+
+@pytest.mark.parametrize("variant", [("1", "64"), ("1", "128"), ("2", "128"), ("2", "192"), ("2", "256")],
+                         ids=lambda v: f"cta{v[0]}-n{v[1]}")
+@pytest.mark.parametrize("fixed", [False, True])
+def test_production_accumulator_is_exact_ladder(cuda, variant, fixed, pair_variant):
+    """K4 on the production kernels (regression for profiles/accwidth_r01.json,
+    which probed the lp_gemm tile kernel): C[r, r] = 2^r unit products + one
+    product of two grid minima (2^-4 * 2^-4) must come out as 2^r + 2^-8
+    exactly for r up to 15 (24 significant bits, the FP8 k-block bound
+    kb <= 2^16).  Every operand is one slice (digits 16 and 1 on the 2^-4 grid),
+    so C = G of the single pair: any truncation inside the tcgen05 FP32
+    accumulation would show, in every kernel variant the planner can pick."""
+    if variant[1] == "256" and not fixed:
+        pytest.skip("256-column tiles are a fixed-step variant")
+    pair_variant(int(variant[0]), int(variant[1]))
+    oz = _oz()
+    R, k = 16, (1 << 15) + 128
+    A = np.zeros((R, k))
+    B = np.zeros((k, R))
+    for r in range(R):
+        A[r, : 1 << r] = 1.0
+        B[: 1 << r, r] = 1.0
+        A[r, k - 1 - r] = 2.0 ** -4
+        B[k - 1 - r, r] = 2.0 ** -4
+    cfg = oz.GemmConfig(oz.get_format("fp8e4m3"), oz.get_format("fp32"),
+                        slice_exponents="fixed" if fixed else "adaptive")
+    res = oz.oz_gemm(A, B, cfg)
+    assert [(b.s_x, b.s_y) for b in res.stats.blocks] == [(1, 1)]
+    want = np.array([2.0 ** r + 2.0 ** -8 for r in range(R)])
+    assert np.array_equal(np.diag(res.C), want), np.diag(res.C) - want
