@@ -531,8 +531,9 @@ __global__ void __launch_bounds__(kThreads, kThreads * kEPT <= 8192 ? 2 : 1) spl
         }
       }
       if (fxa) {
-        // |dg| stays far below the field's headroom: planes <= cap, and every
-        // jump c_p -> c_(p+1) below c_p - w skips only all-zero digit positions.
+        // sh0 is held exactly (<= 1000 < 2^10); dg = c_p - c_0 <= 0 only lowers the
+        // shift, and a shift <= 0 means the residual already lies on the grid
+        // (k is the residual itself, |k| <= 2^(53-rho) by the choice of c_p).
         key = slice_iteration<kThreads, kEPT, kEB, kEmu, true, false, true, true>(
             x, sigma, c - c0, tblc, K, plane, base, t, P.ld, flags, bad, P.pack6, c0 + P.rho - 53);
         if (write && t == 0 && rank == 0) P.expo[(int64_t)it * P.rows + row] = c;
