@@ -519,9 +519,9 @@ def test_tuning_knobs_keep_bits(cuda, kw):
 
 
 def _structured_rows(rng, rows, kb):
-    """Rows that defeat the adaptive split's exponent speculation (a residual max
-    below a quarter of the grid step, early ends, single elements) mixed with
-    random rows."""
+    """Rows whose slice exponents do not follow c_p = c_0 - p (54 - rho) (a
+    residual max below a quarter of the grid step, early ends, single elements)
+    mixed with random rows."""
     X = spread_matrix(rng, rows, kb, 1.0)
     X[0] = 1.0                                   # ends after one slice
     X[1] = 1.0 + 2.0 ** -30                      # residual 2^-30: mismatch at slice 1
@@ -535,12 +535,15 @@ def _structured_rows(rng, rows, kb):
     return X
 
 
-@pytest.mark.parametrize("fmt", ["fp8e4m3", "fp16", "bf16"])
+@pytest.mark.parametrize("fmt", ["fp8e4m3", "fp16", "bf16", "fp6e3m2"])
 @pytest.mark.parametrize("emu", [False, True])
 @pytest.mark.parametrize("kb", [37, 4096, 8192, 20000])
-def test_split_speculation_structured_rows(cuda, fmt, emu, kb):
-    """The batched adaptive split (speculated exponents, one reduction per batch,
-    replay on a mismatch) gives the reference's slices, exponents and counts."""
+def test_split_structured_rows(cuda, fmt, emu, kb):
+    """Adaptive row split on structured rows (early ends, residual maxima far
+    below the grid step so exponents jump, single elements, powers of two,
+    sparse rows) at every launch shape (kb up to 4096, the 256 x 32 / 512 x 16
+    rows, 4-CTA clusters), hardware and emulated (fixed-point residuals): the
+    reference's slices, exponents and counts."""
     import oracle
 
     oz = _oz()
